@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the VCA v2.0 hot path (arxiv 2304.12384) on B200.
+
+Metric (BASELINE.json): UHD 8-bit 4:2:0 frames/sec for the 7 DCT features,
+at 1/2/4/8 GPUs, plus % of roofline.
+
+* N = 1: config 3 -- 600 UHD 8-bit frames, block 32, low-pass (seed 2).
+* N > 1 (torchrun, one rank per GPU, NCCL): config 5's construction, weak
+  scaling -- rank r analyses segment r (600 frames of G(10 + r)) with a
+  one-frame halo (the last frame of segment r - 1) and the per-frame records
+  are gathered to rank 0 over NCCL; at N = 8 this is config 5 exactly.
+
+A step = one vca_analyze over the rank's whole batch (block kernel + finalize
+kernel) [+ the gather for N > 1]; frames are device-resident (7.46 GB per
+GPU, > 126 MB L2, so no L2 flush is needed).  `e2e` repeats the metric
+through vca_analyze_host from pinned host memory (H2D copies and the D2H of
+the records inside the timed region).  `--impl reference` times the CPU
+oracle (test infrastructure) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_FPS = 292.68          # 8-thread SIMD i7-11370H, UHD 8-bit (context only)
+METRIC = "UHD 8-bit 4:2:0 frames/sec (7 DCT features)"
+SEG = 600
+
+
+def frame_bytes(W, H, bd):
+    return (W * H + 2 * (W // 2) * (H // 2)) * (1 if bd == 8 else 2)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload):
+    """Per-launch DRAM bytes of the block kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get(workload)
+        return None if e is None else float(e["dram_bytes_per_frame"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled with NVML every
+    ~5 ms in a thread during the timed region (the recipe's clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.mx = None
+        self.ok = False
+
+    def start(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self.names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                          N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                          N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                          N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                          N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake_slowdown"}
+            self.ok = True
+        except Exception:
+            self.ok = False
+            return
+        self.stop_flag = False
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        N = self.N
+        while not self.stop_flag:
+            try:
+                self.samples.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in self.names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def stop(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_flag = True
+        self.t.join(timeout=2)
+        sm = sorted(self.samples)
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": self.mx, "reasons": sorted(self.reasons), "samples": len(sm)}
+
+
+def bad_clocks(c):
+    if any(r in c["reasons"] for r in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")):
+        return True
+    if c["sm_mhz"] and c["sm_max_mhz"] and c["sm_mhz"] < 0.5 * c["sm_max_mhz"] and "sw_power_cap" not in c["reasons"]:
+        return True
+    return False
+
+
+def cpu_oracle_fps(Y, U, V, bd, block, lowpass, target_s=10.0, max_frames=None):
+    """Time the CPU oracle (as it stands) on a bounded sample; returns (fps, frames, seconds, cores)."""
+    import oracle
+
+    from paper_2304_12384_b200 import synth
+
+    cores = os.cpu_count() or 1
+    npl = synth.as_numpy_planes(Y, U, V)
+    F = npl[0].shape[0]
+    t0 = time.perf_counter()
+    oracle.analyze(npl[0][:1], npl[1][:1], npl[2][:1], bd, block, lowpass, n_threads=1)
+    one = time.perf_counter() - t0
+    n = max(1, min(F, int(target_s * cores / max(one, 1e-3))))
+    if max_frames:
+        n = min(n, max_frames)
+    t0 = time.perf_counter()
+    oracle.analyze(npl[0][:n], npl[1][:n], npl[2][:n], bd, block, lowpass, n_threads=cores)
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt, cores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the box's host cores, rank 0 only."""
+    if rank != 0:
+        return 0
+    import oracle
+
+    from paper_2304_12384_b200 import synth
+
+    oracle.build()
+    c = synth.CONFIGS[3]
+    cores = os.cpu_count() or 1
+    # bounded sample of the workload: one frame per host core per step
+    n = max(1, min(cores, 16))
+    Y, U, V = synth.config_frames(3, device="cpu", n_frames=n)
+    npl = synth.as_numpy_planes(Y, U, V)
+    for _ in range(args.warmup):
+        oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_threads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_threads=cores)
+    dt = time.perf_counter() - t0
+    fps = n * args.steps / dt
+    sample = "%d UHD frames of config 3 per step (one per host core), oracle OpenMP over frames" % n
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic (config 3 generator G(2), CPU torch)",
+        "config": {"workload": "config3_uhd_8bit_lowpass32 (bounded sample)", "width": c.width,
+                   "height": c.height, "bit_depth": 8, "block": 32, "lowpass": True, "frames_per_step": n},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "paper_context_fps": PAPER_FPS,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--frames", type=int, default=SEG, help="frames per GPU (default 600)")
+    ap.add_argument("--config", type=int, default=0, help="override workload config (1-4; N=1 only)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg")
+    ap.add_argument("--e2e-frames", type=int, default=120)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_12384_b200 import Analyzer, records_to_numpy, synth
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg_id = args.config or 3
+    c = synth.CONFIGS[cfg_id]
+    W, H, bd = c.width, c.height, c.bit_depth
+    F = args.frames
+    # --- inputs (outside timing): rank r = segment r of config 5 for N > 1
+    if world == 1:
+        Y, U, V = synth.config_frames(cfg_id, device=dev, n_frames=F)
+        n_halo = 0
+        workload = "config%d_%s_%df" % (cfg_id, c.name, F)
+        first_poc = 0
+    else:
+        n_halo = 1 if rank > 0 else 0
+        first = rank * SEG - n_halo
+        Y, U, V = synth.config_frames(5, device=dev, n_frames=F + n_halo, first_t=first)
+        workload = "config5_%s_%dx%df" % (synth.CONFIGS[5].name, world, F)
+        first_poc = rank * SEG
+    torch.cuda.synchronize()
+
+    an = Analyzer(W, H, bd, c.block_size, c.lowpass)
+    nfr = Y.shape[0]
+    out = torch.empty((nfr - n_halo, 8), dtype=torch.float64, device=dev)
+    scratch = torch.empty(an.scratch_bytes(nfr) // 8 + 1, dtype=torch.float64, device=dev)
+    gathered = torch.empty((world * (nfr - n_halo), 8), dtype=torch.float64, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        an.reset(first_poc)
+        an.analyze(Y, U, V, n_halo=n_halo, out=out, scratch=scratch, stream=stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    an.profile_read()  # reset counters
+
+    def timed():
+        an.profile_enable(True)
+        clk = ClockSampler(local)
+        clk.start()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = clk.stop()
+        an.profile_enable(False)
+        ms = e0.elapsed_time(e1)
+        blk_ms, fin_ms, launches = an.profile_read()
+        return ms, blk_ms, fin_ms, launches, clocks
+
+    ms, blk_ms, fin_ms, launches, clocks = timed()
+    remeasured = False
+    if bad_clocks(clocks):
+        remeasured = True
+        ms, blk_ms, fin_ms, launches, clocks = timed()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    frames_total = world * (nfr - n_halo) if world > 1 else nfr
+    value = frames_total * args.steps / (ms / 1e3)
+    fb = frame_bytes(W, H, bd)
+    peak, peak_src = load_peaks()
+    per_launch_s = blk_ms / 1e3 / args.steps
+    achieved = nfr * fb / per_launch_s / 1e9
+    traffic_pf = load_traffic(workload.split("_")[0] if world == 1 else "config5")
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 in; s8xu8->s32 DCT, f64 features",
+        "data": "synthetic, seeded (paper_2304_12384_b200/synth.py), device-resident",
+        "config": {"workload": workload, "width": W, "height": H, "bit_depth": bd, "block": c.block_size,
+                   "lowpass": c.lowpass, "frames_per_gpu": nfr - n_halo, "halo_frames": n_halo,
+                   "path": an.info["path"], "parallelism": "frame-range dp%d + halo + NCCL all_gather" % world
+                   if world > 1 else "single GPU",
+                   "l2": "inputs %.2f GB per GPU > 126 MB L2; no flush needed" % (nfr * fb / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None if traffic_pf is None else traffic_pf * nfr,
+                     "kernel": "block kernel (A1-A7), CUDA events on the launching stream",
+                     "algorithmic_bytes_per_launch": nfr * fb, "peak_source": peak_src,
+                     "kernel_ms_per_launch": per_launch_s * 1e3, "finalize_ms_per_launch": fin_ms / args.steps,
+                     "roofline_fps": peak * 1e9 / fb},
+        "gpu_launches": int(launches),
+        "clocks": {**clocks, "remeasured": remeasured},
+        "paper_context_fps": PAPER_FPS,
+    }
+
+    # --- e2e through the public host API (pinned host frames, H2D + D2H inside the timed region)
+    if not args.no_e2e:
+        ne = min(args.e2e_frames, nfr)
+        hY, hU, hV = (p[:ne].cpu().pin_memory() for p in (Y, U, V))
+        ae = Analyzer(W, H, bd, c.block_size, c.lowpass)
+        ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=8)  # warm-up / staging allocation
+        if world > 1:
+            dist.barrier()
+        e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            ae.reset(first_poc)
+            ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=8)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        fr = (world if world > 1 else 1) * (ne - n_halo)
+        line["e2e"] = {"value": fr * e_steps / dt, "unit": "frames/s", "h2d_bytes_per_step": ne * fb,
+                       "d2h_bytes_per_step": (ne - n_halo) * 64, "frames_per_step": ne,
+                       "api": "vca_analyze_host (pinned host memory, 8-frame chunks, copy/compute overlap)"}
+        del hY, hU, hV, ae
+
+    # --- CPU oracle baseline, rank 0 at N = 1 only
+    if world == 1 and not args.no_cpu:
+        ns = min(nfr, 160)
+        fps, n, dt, cores = cpu_oracle_fps(Y[:ns].cpu(), U[:ns].cpu(), V[:ns].cpu(), bd, c.block_size, c.lowpass)
+        line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                                "sample": "%d frames of the same workload, %.1f s, OpenMP over frames" % (n, dt)}
+    if rank == 0:
+        # parity spot check of the timed output (first and last record) is done in tests; here sanity only
+        rec = records_to_numpy(gathered if world > 1 else out)
+        line["sanity"] = {"records": int(len(rec)), "first_poc": int(rec["poc"][0]), "last_poc": int(rec["poc"][-1]),
+                          "mean_E_Y": float(rec["E_Y"].mean())}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -180,3 +180,18 @@ def as_numpy_planes(Y, U, V):
             a = a.view(np.uint16)
         res.append(a)
     return tuple(res)
+
+
+def with_pitch(planes, align: int = 16):
+    """Copy [F][H][W] planes into buffers whose row pitch is rounded up to
+    ``align`` bytes (libvca requires 16-byte aligned pitches), returning
+    strided views of the same shape."""
+    res = []
+    for p in planes:
+        F, H, W = p.shape
+        es = p.element_size()
+        wp = ((W * es + align - 1) // align * align) // es
+        buf = torch.zeros((F, H, wp), dtype=p.dtype, device=p.device)
+        buf[:, :, :W] = p
+        res.append(buf[:, :, :W])
+    return tuple(res)

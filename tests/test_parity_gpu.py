@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded bytes.  Bar (BASELINE.json north star; R-11): integer DCT
+coefficients and DC sums bit-exact; per-frame features within 1e-6 relative,
+an exact 0 reproduced as exactly 0."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2304_12384_b200 import Analyzer, records_to_numpy, synth
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-6
+FEATS = ("E_Y", "h", "L_Y", "E_U", "L_U", "E_V", "L_V")
+
+
+def assert_records(gpu, ref, rtol=RTOL):
+    assert len(gpu) == len(ref)
+    assert np.array_equal(gpu["poc"], ref["poc"])
+    for f in FEATS:
+        g, r = gpu[f], ref[f]
+        zero = r == 0.0
+        assert np.all(g[zero] == 0.0), f
+        rel = np.abs(g[~zero] - r[~zero]) / np.abs(r[~zero])
+        assert rel.size == 0 or rel.max() <= rtol, (f, float(rel.max()))
+
+
+def planes_cuda(Y, U, V):
+    """Device copies with 16-byte-aligned row pitch (libvca contract)."""
+    return synth.with_pitch(tuple(p.cuda() for p in (Y, U, V)))
+
+
+def run_both(Y, U, V, bd, w, lp, n_halo=0):
+    """Y, U, V torch CPU tensors -> (gpu records, oracle records)."""
+    a = Analyzer(Y.shape[2], Y.shape[1], bd, w, lp)
+    rec = a.analyze(*planes_cuda(Y, U, V), n_halo=n_halo)
+    torch.cuda.synchronize()
+    g = records_to_numpy(rec)
+    r = oracle.analyze(*synth.as_numpy_planes(Y, U, V), bd, w, lp, n_halo=n_halo)
+    return g, r, a
+
+
+def check_dump(a, Y, U, V, bd, w, lp, frame=0):
+    """Bit-exact coefficients / DC sums / per-block H, L of one frame."""
+    dump = a.debug_dump(*planes_cuda(Y[frame:frame + 1], U[frame:frame + 1], V[frame:frame + 1]))
+    npl = synth.as_numpy_planes(Y[frame:frame + 1], U[frame:frame + 1], V[frame:frame + 1])
+    info = a.info
+    for p in range(3):
+        plane = npl[p][0]
+        wp, n = info["block"][p], info["n"][p]
+        k = 0
+        for r in range(info["rows"][p]):
+            for c in range(info["cols"][p]):
+                C, sumx, H, L = oracle.block(plane, bd, wp, lp, r, c)
+                got = dump[p]["coeffs"][k].astype(np.int64)
+                want = C.copy()
+                want[0, 0] = np.int64(np.uint32(want[0, 0] & 0xFFFFFFFF).view(np.int32))  # C_00 mod 2^32 (R-11)
+                assert np.array_equal(got, want), (p, r, c)
+                assert dump[p]["sumx"][k] == sumx and 4096 * sumx == C[0, 0]
+                assert dump[p]["L"][k] == L                      # same correctly-rounded sqrt
+                assert abs(dump[p]["H"][k] - H) <= 1e-12 * max(H, 1e-300)
+                k += 1
+
+
+CASES = [
+    # (name, W, H, bit depth, block, lowpass)  -- small geometries spanning several tiles + ragged tails
+    ("cif_full32", 352, 288, 8, 32, False),           # config 1 geometry
+    ("ragged_full32", 200, 136, 8, 32, False),        # config 2 family: partial last row AND column
+    ("ragged_lp32", 264, 176, 8, 32, True),           # config 3 family: last row 16/32
+    ("ragged_10bit_full16", 136, 100, 10, 16, False),  # config 4 family
+    ("lp32_10bit", 128, 96, 10, 32, True),
+    ("full16_8bit", 160, 88, 8, 16, False),
+    ("lp16", 96, 72, 8, 16, True),                     # generic kernel: n = 8 / 4
+    ("full8", 72, 46, 8, 8, False),
+    ("full4", 38, 22, 8, 4, False),                    # chroma grid differs from luma grid
+    ("full4_10bit", 40, 24, 10, 4, False),
+    ("tiny_8x8", 8, 8, 8, 32, False),                  # plane smaller than a block
+]
+
+
+@pytest.mark.parametrize("name,W,H,bd,w,lp", CASES, ids=[c[0] for c in CASES])
+def test_parity_small(name, W, H, bd, w, lp):
+    F = 4
+    Y, U, V = synth.g_frames(17, W, H, F, bd)
+    g, r, a = run_both(Y, U, V, bd, w, lp)
+    assert_records(g, r)
+    check_dump(a, Y, U, V, bd, w, lp, frame=1)
+
+
+def test_parity_config1_cif_all_frames():
+    Y, U, V = synth.config_frames(1)
+    g, r, a = run_both(Y, U, V, 8, 32, False)
+    assert_records(g, r)
+    for t in range(0, 16, 5):
+        check_dump(a, Y, U, V, 8, 32, False, frame=t)
+
+
+def test_extreme_values():
+    """Saturated / zero / checkerboard frames: exact zeros, int32 headroom at 10-bit (R-11)."""
+    for bd, w, lp in ((8, 32, False), (10, 16, False), (8, 32, True), (10, 32, True), (10, 8, False)):
+        hi = (1 << bd) - 1
+        dt = torch.uint8 if bd == 8 else torch.int16
+        W, H = 96, 64
+        yy, xx = torch.meshgrid(torch.arange(H), torch.arange(W), indexing="ij")
+        cb = ((xx + yy) % 2) * hi
+        frames = [torch.zeros(H, W), torch.full((H, W), float(hi)), cb.float(), torch.zeros(H, W)]
+        Y = torch.stack(frames).to(dt)
+        U = torch.stack([f[: H // 2, : W // 2] for f in frames]).to(dt)
+        V = torch.stack([f[: H // 2, : W // 2].flip(1) for f in frames]).to(dt)
+        g, r, a = run_both(Y, U, V, bd, w, lp)
+        assert_records(g, r)
+        assert g["E_Y"][0] == 0.0 and g["h"][1] == 0.0 and g["L_Y"][0] == 0.0
+        check_dump(a, Y, U, V, bd, w, lp, frame=2)
+
+
+def test_ten_bit_clamp_gpu():
+    """container values > 1023 are clamped (kernel and oracle alike)."""
+    Y, U, V = synth.g_frames(3, 64, 48, 2, 10)
+    Y[0, 5, 7] = 4000
+    U[1, 3, 3] = 2000
+    g, r, _ = run_both(Y, U, V, 10, 16, False)
+    assert_records(g, r)
+
+
+def test_split_and_halo_invariance():
+    """S:362/S:379 analog: any chunking of the sequence into calls (carried
+    H_Y) or a range split with a one-frame halo is bit-identical."""
+    Y, U, V = planes_cuda(*synth.g_frames(23, 264, 176, 9, 8))  # 264: pitch 272 (padded)
+    a = Analyzer(264, 176, 8, 32, True)
+    whole = records_to_numpy(a.analyze(Y, U, V))
+    b = Analyzer(264, 176, 8, 32, True)
+    parts = []
+    for s, e in ((0, 2), (2, 3), (3, 9)):
+        parts.append(records_to_numpy(b.analyze(Y[s:e], U[s:e], V[s:e])))
+    assert np.array_equal(np.concatenate(parts), whole)
+    # two "ranks": [0, 5) and [5, 9) with halo frame 4
+    c = Analyzer(264, 176, 8, 32, True)
+    c.reset(5)
+    tail = records_to_numpy(c.analyze(Y[4:], U[4:], V[4:], n_halo=1))
+    assert np.array_equal(tail, whole[5:])
+    # reset starts a new sequence: h = 0
+    b.reset(0)
+    again = records_to_numpy(b.analyze(Y[3:5], U[3:5], V[3:5]))
+    assert again["h"][0] == 0.0 and again["poc"][0] == 0
+
+
+def test_analyze_host_matches_device():
+    Yc, Uc, Vc = synth.with_pitch(synth.g_frames(31, 200, 136, 7, 8))
+    Yp, Up, Vp = (torch.empty_strided(p.shape, p.stride(), dtype=p.dtype, pin_memory=True) for p in (Yc, Uc, Vc))
+    for d, s_ in zip((Yp, Up, Vp), (Yc, Uc, Vc)):
+        d.copy_(s_)
+    a = Analyzer(200, 136, 8, 32, False)
+    dev = records_to_numpy(a.analyze(*planes_cuda(Yc, Uc, Vc)))
+    b = Analyzer(200, 136, 8, 32, False)
+    host = b.analyze_host(Yp, Up, Vp, chunk_frames=3)
+    assert np.array_equal(host, dev)
+    c = Analyzer(200, 136, 8, 32, False)
+    host2 = c.analyze_host(Yc, Uc, Vc, n_halo=1, chunk_frames=2)  # pageable memory, halo
+    assert np.array_equal(host2[1:], dev[2:])
+
+
+def test_argument_errors_gpu():
+    from paper_2304_12384_b200 import VcaError
+
+    a = Analyzer(64, 64, 8, 32, False)
+    Y = torch.zeros((2, 64, 64), dtype=torch.uint8, device="cuda")
+    U = torch.zeros((2, 32, 32), dtype=torch.uint8, device="cuda")
+    with pytest.raises(VcaError) as e:
+        a.analyze(Y[:, :, 1:], U, U)           # misaligned base (and pitch < row bytes is not the issue)
+    assert e.value.code in (-6, -1)
+    with pytest.raises(VcaError) as e:
+        a.analyze(Y[:1], U[:1], U[:1], n_halo=1)  # n_frames < 1 + n_halo
+    assert e.value.code == -1
+    small = torch.empty(1, dtype=torch.float64, device="cuda")
+    with pytest.raises(VcaError) as e:
+        a.analyze(Y, U, U, scratch=small)
+    assert e.value.code == -9
+    # the context is still usable after argument errors
+    rec = records_to_numpy(a.analyze(Y, U, U))
+    assert np.all(rec["E_Y"] == 0.0)
+
+
+def test_profile_counters():
+    a = Analyzer(128, 64, 8, 32, True)
+    Y, U, V = planes_cuda(*synth.g_frames(1, 128, 64, 3, 8))
+    a.profile_enable(True)
+    a.analyze(Y, U, V)
+    a.analyze(Y, U, V)
+    blk, fin, launches = a.profile_read()
+    assert blk > 0 and fin > 0 and launches == 4
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", (2, 3, 4))
+def test_parity_full_size_sampled(cfg):
+    """Full BASELINE.json geometry, analysed in one call over many frames (the
+    launch configuration bench.py times); sampled frames checked against the
+    oracle (records incl. h via a halo frame, and the coefficient dump)."""
+    c = synth.CONFIGS[cfg]
+    F = 24
+    Y, U, V = synth.config_frames(cfg, device="cuda", n_frames=F)
+    a = Analyzer(c.width, c.height, c.bit_depth, c.block_size, c.lowpass)
+    g = records_to_numpy(a.analyze(Y, U, V))
+    for t in (1, F - 1):
+        npl = synth.as_numpy_planes(Y[t - 1:t + 1], U[t - 1:t + 1], V[t - 1:t + 1])
+        r = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=1, first_poc=t)
+        assert_records(g[t:t + 1], r)
+    Yc, Uc, Vc = (p[F - 1:F].cpu() for p in (Y, U, V))
+    check_dump(a, Yc, Uc, Vc, c.bit_depth, c.block_size, c.lowpass, frame=0)
