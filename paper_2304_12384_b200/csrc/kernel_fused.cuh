@@ -1,17 +1,790 @@
-// kernel_fused.cuh -- placeholder until the fused tensor-core kernel lands.
+// kernel_fused.cuh -- the fused hot-path kernel (A1-A7) for the block
+// configurations of BASELINE.json: luma block w in {16, 32}, chroma block
+// w/2 on the same block grid, 8- or 10-bit, full or low-pass.
+//
+// One work item = one block row r of one frame f.  A persistent CTA walks its
+// items strip by strip; a strip is 4 horizontally adjacent units, a unit being
+// the co-located Y block (w x w) and U, V blocks (w/2 x w/2) of (f, r, c).
+//
+//  * warp 0 (one elected lane) is the TMA producer: per strip it issues one
+//    3-D tensor-map load per plane box (swizzled, zero-filled out of bounds)
+//    into a ring of smem stages guarded by full/empty mbarriers (A1);
+//  * warps 1..4 are consumers, warp 1+u owning unit 4s+u of strip s.  A
+//    consumer reads its unit from smem with clamped row/column indices (edge
+//    replication, A2), low-pass-downsamples in registers with
+//    (s+2)>>2 (A3, R-5), and runs the exact integer DCT C = T X T^T on the
+//    tensor cores (A4, R-1) as two int8 IMMA passes that never leave
+//    registers:
+//        pass 1   Z^T = T . X^T      (s8 basis x u8 pixels -> s32)
+//        pass 2   C   = T' . Z'      with Z split into 3 byte planes
+//                 (u8, u8, s8) and C = D0 + 2^8 D1 + 2^16 D2 (mod 2^32);
+//    the C-fragment layout of pass 1 is, up to a fixed permutation pi of the
+//    contraction index y, the B-fragment layout of pass 2, so T' = T[:, pi]
+//    (a constant) absorbs the transpose -- no shuffles, no smem round trip.
+//    10-bit samples enter pass 1 as two byte planes (lo, hi).
+//    Chroma 8x8 DCTs pair U and V block-diagonally into one 16x16 MMA.
+//  * the FP64 epilogue (A5, A6, R-2, R-3) weighs |C_ij| by the
+//    per-lane-constant w_n(i,j)/(4096 n), reduces the luma H per unit (needed
+//    per block for h) and U/V H per item, and writes per-(frame, row, warp)
+//    partial sums in a fixed order (A7 inputs, R-11).
 #pragma once
+#include <cuda.h>
+
 #include "kernel_generic.cuh"
 #include "vca_common.cuh"
 
 namespace vca {
 
-inline bool fused_supported(int /*w*/, int /*lowpass*/, bool /*grids_equal*/) { return false; }
-inline int fused_partials_per_row() { return 1; }
-inline cudaError_t fused_prepare(int, int, int) { return cudaSuccess; }
-inline int launch_fused(const Planes3 &, int, int, int, const int8_t *, const double *, const Scratch &,
-                        const DumpPtrs &, int, cudaStream_t)
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
-    return -1;
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "VCA_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra VCA_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y, int z,
+                                            uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// D = A(s8) . B(u8) + C, m16n8k16
+__device__ __forceinline__ void mma16_su(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b)
+{
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+                 : "r"(a0), "r"(a1), "r"(b), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mma16_ss(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b)
+{
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+                 : "r"(a0), "r"(a1), "r"(b), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+// m16n8k32
+__device__ __forceinline__ void mma32_su(int32_t (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mma32_ss(int32_t (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+
+// byte planes b = 0, 1, 2 of four int32 values (v0..v3 -> bytes 0..3 of each plane)
+__device__ __forceinline__ void byte_planes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t &p0,
+                                            uint32_t &p1, uint32_t &p2)
+{
+    const uint32_t s0 = __byte_perm(v0, v1, 0x5140);  // v0.b0 v1.b0 v0.b1 v1.b1
+    const uint32_t s1 = __byte_perm(v0, v1, 0x7362);  // v0.b2 v1.b2 v0.b3 v1.b3
+    const uint32_t s2 = __byte_perm(v2, v3, 0x5140);
+    const uint32_t s3 = __byte_perm(v2, v3, 0x7362);
+    p0 = __byte_perm(s0, s2, 0x5410);
+    p1 = __byte_perm(s0, s2, 0x7632);
+    p2 = __byte_perm(s1, s3, 0x5410);
+}
+
+// |C| as an exact double: 2^52 + u reinterpreted, minus 2^52 (one DADD)
+__device__ __forceinline__ double abs_to_double(int32_t c)
+{
+    const uint32_t u = (uint32_t)(c < 0 ? -c : c);
+    return __hiloint2double(0x43300000, (int)u) - 4503599627370496.0;
+}
+
+__device__ __forceinline__ int32_t combine3(int32_t d0, int32_t d1, int32_t d2)
+{
+    return (int32_t)((uint32_t)d0 + ((uint32_t)d1 << 8) + ((uint32_t)d2 << 16));
+}
+
+// ------------------------------------------------------------------ family geometry
+template <int W_, int BD_, int LP_>
+struct Fam {
+    static constexpr int W = W_, WC = W_ / 2, BD = BD_, LP = LP_;
+    static constexpr int ES = BD == 8 ? 1 : 2;
+    static constexpr int NY = LP ? W / 2 : W;
+    static constexpr int NC = LP ? WC / 2 : WC;
+    static constexpr int UNITS = 4;                        // units per strip (= consumer warps)
+    static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
+    static constexpr int IB_Y = (UNITS * RB_Y) < 128 ? UNITS * RB_Y : 128;  // box inner bytes = swizzle span
+    static constexpr int IB_C = (UNITS * RB_C) < 128 ? UNITS * RB_C : 128;
+    static constexpr int UPB_Y = IB_Y / RB_Y, UPB_C = IB_C / RB_C;        // units per box
+    static constexpr int NBOX_Y = UNITS / UPB_Y, NBOX_C = UNITS / UPB_C;
+    static constexpr int BOXB_Y = IB_Y * W, BOXB_C = IB_C * WC;            // bytes per box
+    static constexpr int ST_Y = NBOX_Y * BOXB_Y, ST_C = NBOX_C * BOXB_C;
+    static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
+    static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
+    static constexpr int STAGES = (49152 / STAGE) < 4 ? 4 : (49152 / STAGE > 16 ? 16 : 49152 / STAGE);
+    static constexpr bool WTAB = (NY == 32);               // luma weights from smem (32 per lane)
+    static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0);
+    static_assert(NC == NY / 2, "chroma DCT is half the luma DCT");
+    static_assert(IB_Y == 32 || IB_Y == 64 || IB_Y == 128, "swizzle span");
+    static_assert(IB_C == 32 || IB_C == 64 || IB_C == 128, "swizzle span");
+};
+
+template <int IB>
+__device__ __forceinline__ uint32_t swz(uint32_t off)
+{
+    constexpr uint32_t m = IB / 16 - 1;   // 128B: bits 4-6 ^= bits 7-9; 64B: 4-5 ^= 7-8; 32B: 4 ^= 7
+    return off ^ (((off >> 7) & m) << 4);
+}
+
+// One sample of a unit in a swizzled box (row, column within the unit), 10-bit clamp
+template <int ES, int IB>
+__device__ __forceinline__ int box_sample(const uint8_t *box, int ub0, int row, int xs)
+{
+    if (ES == 1) return box[swz<IB>(row * IB + ub0 + xs)];
+    const int v = *reinterpret_cast<const uint16_t *>(box + swz<IB>(row * IB + ub0 + 2 * xs));
+    return v < 1023 ? v : 1023;
+}
+
+// 8-bit 2x2 low-pass of two source rows of 8 bytes -> 4 packed outputs, (s+2)>>2 (R-5)
+__device__ __forceinline__ uint32_t ds8(uint2 a, uint2 b)
+{
+    const uint32_t M = 0x00FF00FFu;
+    const uint32_t sl = (a.x & M) + ((a.x >> 8) & M) + (b.x & M) + ((b.x >> 8) & M) + 0x00020002u;
+    const uint32_t sh = (a.y & M) + ((a.y >> 8) & M) + (b.y & M) + ((b.y >> 8) & M) + 0x00020002u;
+    return __byte_perm((sl >> 2) & M, (sh >> 2) & M, 0x6420);
+}
+
+__device__ __forceinline__ uint32_t pair_sum16(uint32_t v)
+{
+    return (v & 0xFFFFu) + (v >> 16);
+}
+
+// Four consecutive DCT-input samples x = 4xg..4xg+3 of row y of one unit, as
+// byte planes lo (and hi for 10-bit).  hv/wv: valid rows/columns of the unit in
+// source samples (edge replication by clamping); xpart: wv < block width.
+template <class F, int PL>
+__device__ __forceinline__ void load4(const uint8_t *box, int ub, int y, int xg, int hv, int wv, bool xpart,
+                                      uint32_t &lo, uint32_t &hi)
+{
+    constexpr int IB = PL == 0 ? F::IB_Y : F::IB_C;
+    constexpr int RB = PL == 0 ? F::RB_Y : F::RB_C;
+    constexpr int ES = F::ES;
+    const int ub0 = ub * RB;
+    if (!xpart) {
+        if (!F::LP) {
+            const int row = min(y, hv - 1);
+            if (ES == 1) {
+                lo = *reinterpret_cast<const uint32_t *>(box + swz<IB>(row * IB + ub0 + 4 * xg));
+                hi = 0;
+            } else {
+                uint2 v = *reinterpret_cast<const uint2 *>(box + swz<IB>(row * IB + ub0 + 8 * xg));
+                v.x = __vminu2(v.x, 0x03FF03FFu);
+                v.y = __vminu2(v.y, 0x03FF03FFu);
+                lo = __byte_perm(v.x, v.y, 0x6420);
+                hi = __byte_perm(v.x, v.y, 0x7531);
+            }
+        } else {
+            const int r0 = min(2 * y, hv - 1), r1 = min(2 * y + 1, hv - 1);
+            if (ES == 1) {
+                const uint2 a = *reinterpret_cast<const uint2 *>(box + swz<IB>(r0 * IB + ub0 + 8 * xg));
+                const uint2 b = *reinterpret_cast<const uint2 *>(box + swz<IB>(r1 * IB + ub0 + 8 * xg));
+                lo = ds8(a, b);
+                hi = 0;
+            } else {
+                uint4 a = *reinterpret_cast<const uint4 *>(box + swz<IB>(r0 * IB + ub0 + 16 * xg));
+                uint4 b = *reinterpret_cast<const uint4 *>(box + swz<IB>(r1 * IB + ub0 + 16 * xg));
+                const uint32_t C10 = 0x03FF03FFu;
+                const uint32_t d0 = (pair_sum16(__vminu2(a.x, C10)) + pair_sum16(__vminu2(b.x, C10)) + 2) >> 2;
+                const uint32_t d1 = (pair_sum16(__vminu2(a.y, C10)) + pair_sum16(__vminu2(b.y, C10)) + 2) >> 2;
+                const uint32_t d2 = (pair_sum16(__vminu2(a.z, C10)) + pair_sum16(__vminu2(b.z, C10)) + 2) >> 2;
+                const uint32_t d3 = (pair_sum16(__vminu2(a.w, C10)) + pair_sum16(__vminu2(b.w, C10)) + 2) >> 2;
+                const uint32_t p01 = d0 | (d1 << 16), p23 = d2 | (d3 << 16);
+                lo = __byte_perm(p01, p23, 0x6420);
+                hi = __byte_perm(p01, p23, 0x7531);
+            }
+        }
+    } else {  // partial last block column: per-sample clamped reads
+        uint32_t l = 0, h = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int x = 4 * xg + k;
+            int v;
+            if (!F::LP) {
+                v = box_sample<ES, IB>(box, ub0, min(y, hv - 1), min(x, wv - 1));
+            } else {
+                const int r0 = min(2 * y, hv - 1), r1 = min(2 * y + 1, hv - 1);
+                const int x0 = min(2 * x, wv - 1), x1 = min(2 * x + 1, wv - 1);
+                v = (box_sample<ES, IB>(box, ub0, r0, x0) + box_sample<ES, IB>(box, ub0, r0, x1) +
+                     box_sample<ES, IB>(box, ub0, r1, x0) + box_sample<ES, IB>(box, ub0, r1, x1) + 2) >> 2;
+            }
+            l |= (uint32_t)(v & 255) << (8 * k);
+            h |= (uint32_t)(v >> 8) << (8 * k);
+        }
+        lo = l;
+        hi = h;
+    }
+}
+
+// ------------------------------------------------------------------ per-lane constant fragments
+struct LaneConst {
+    // n = 16 (m16n8k16): pass-1 A = T16, pass-2 A = T16[:, pi16]
+    uint32_t t16a0, t16a1, p16a0, p16a1;
+    // paired n = 8: pass-1 A = blockdiag(T8, T8), pass-2 A = blockdiag permuted
+    uint32_t t8a0, t8a1, p8a0, p8a1;
+    // n = 32 (m16n8k32), per m-tile
+    uint32_t t32[2][4], p32[2][4];
+};
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d)
+{
+    return (uint32_t)(a & 255) | ((uint32_t)(b & 255) << 8) | ((uint32_t)(c & 255) << 16) | ((uint32_t)(d & 255) << 24);
+}
+
+// pi16(k): slot k = 4t' + i' of pass 2 carries y = 8(i'>>1) + 2t' + (i'&1)
+__device__ __forceinline__ int pi16(int k) { return 8 * ((k & 3) >> 1) + 2 * (k >> 2) + (k & 1); }
+// pi32(k): k = 16h + 4t' + i' -> 16h + 8(i'>>1) + 2t' + (i'&1)
+__device__ __forceinline__ int pi32(int k) { return 16 * (k >> 4) + pi16(k & 15); }
+
+__device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all, int g, int t, int NY)
+{
+    if (NY == 16 || NY == 32) {
+        const int8_t *T16 = T_all + table_offset(16);
+        const int8_t *T8 = T_all + table_offset(8);
+        auto T16a = [&](int i, int x) { return (int)__ldg(T16 + i * 16 + x); };
+        auto T8a = [&](int i, int x) { return (int)__ldg(T8 + i * 8 + x); };
+        L.t16a0 = pack4(T16a(g, 4 * t), T16a(g, 4 * t + 1), T16a(g, 4 * t + 2), T16a(g, 4 * t + 3));
+        L.t16a1 = pack4(T16a(g + 8, 4 * t), T16a(g + 8, 4 * t + 1), T16a(g + 8, 4 * t + 2), T16a(g + 8, 4 * t + 3));
+        L.p16a0 = pack4(T16a(g, pi16(4 * t)), T16a(g, pi16(4 * t + 1)), T16a(g, pi16(4 * t + 2)),
+                        T16a(g, pi16(4 * t + 3)));
+        L.p16a1 = pack4(T16a(g + 8, pi16(4 * t)), T16a(g + 8, pi16(4 * t + 1)), T16a(g + 8, pi16(4 * t + 2)),
+                        T16a(g + 8, pi16(4 * t + 3)));
+        // blockdiag(T8, T8): rows 0-7 (U) act on k 0-7, rows 8-15 (V) on k 8-15
+        const int xb = 4 * (t & 1);
+        const uint32_t row = pack4(T8a(g, xb), T8a(g, xb + 1), T8a(g, xb + 2), T8a(g, xb + 3));
+        L.t8a0 = t < 2 ? row : 0u;
+        L.t8a1 = t < 2 ? 0u : row;
+        // pass 2: slot 4t+i carries (block (i>>1): 0 = U, 1 = V, y = 2t + (i&1))
+        int u[4], v[4];
+        for (int i = 0; i < 4; ++i) {
+            const int y = 2 * t + (i & 1);
+            const bool isV = (i >> 1) != 0;
+            u[i] = isV ? 0 : T8a(g, y);
+            v[i] = isV ? T8a(g, y) : 0;
+        }
+        L.p8a0 = pack4(u[0], u[1], u[2], u[3]);
+        L.p8a1 = pack4(v[0], v[1], v[2], v[3]);
+    }
+    if (NY == 32) {
+        const int8_t *T32 = T_all + table_offset(32);
+        auto T32a = [&](int i, int x) { return (int)__ldg(T32 + i * 32 + x); };
+        for (int mt = 0; mt < 2; ++mt) {
+            const int r0 = 16 * mt + g, r1 = r0 + 8;
+            L.t32[mt][0] = pack4(T32a(r0, 4 * t), T32a(r0, 4 * t + 1), T32a(r0, 4 * t + 2), T32a(r0, 4 * t + 3));
+            L.t32[mt][1] = pack4(T32a(r1, 4 * t), T32a(r1, 4 * t + 1), T32a(r1, 4 * t + 2), T32a(r1, 4 * t + 3));
+            L.t32[mt][2] = pack4(T32a(r0, 16 + 4 * t), T32a(r0, 17 + 4 * t), T32a(r0, 18 + 4 * t), T32a(r0, 19 + 4 * t));
+            L.t32[mt][3] = pack4(T32a(r1, 16 + 4 * t), T32a(r1, 17 + 4 * t), T32a(r1, 18 + 4 * t), T32a(r1, 19 + 4 * t));
+            L.p32[mt][0] = pack4(T32a(r0, pi32(4 * t)), T32a(r0, pi32(4 * t + 1)), T32a(r0, pi32(4 * t + 2)),
+                                 T32a(r0, pi32(4 * t + 3)));
+            L.p32[mt][1] = pack4(T32a(r1, pi32(4 * t)), T32a(r1, pi32(4 * t + 1)), T32a(r1, pi32(4 * t + 2)),
+                                 T32a(r1, pi32(4 * t + 3)));
+            L.p32[mt][2] = pack4(T32a(r0, pi32(16 + 4 * t)), T32a(r0, pi32(17 + 4 * t)), T32a(r0, pi32(18 + 4 * t)),
+                                 T32a(r0, pi32(19 + 4 * t)));
+            L.p32[mt][3] = pack4(T32a(r1, pi32(16 + 4 * t)), T32a(r1, pi32(17 + 4 * t)), T32a(r1, pi32(18 + 4 * t)),
+                                 T32a(r1, pi32(19 + 4 * t)));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ DCT building blocks
+// n = 16: B fragments (lo/hi) for pass-1 n-tiles q = 0, 1 (y = 8q + g, x = 4t..4t+3)
+// -> C[p][e]: i = g + 8(e>>1), j = 8p + 2t + (e&1).
+template <int ES>
+__device__ __forceinline__ void dct16(const LaneConst &L, const uint32_t (&blo)[2], const uint32_t (&bhi)[2],
+                                      int32_t (&C)[2][4])
+{
+    int32_t D1[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        mma16_su(D1[q], L.t16a0, L.t16a1, blo[q]);
+        if (ES == 2) {
+            int32_t Dh[4];
+            mma16_su(Dh, L.t16a0, L.t16a1, bhi[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) D1[q][e] = (int32_t)((uint32_t)D1[q][e] + ((uint32_t)Dh[e] << 8));
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        uint32_t b0, b1, b2;
+        byte_planes(D1[0][2 * p], D1[0][2 * p + 1], D1[1][2 * p], D1[1][2 * p + 1], b0, b1, b2);
+        int32_t E0[4], E1[4], E2[4];
+        mma16_su(E0, L.p16a0, L.p16a1, b0);
+        mma16_su(E1, L.p16a0, L.p16a1, b1);
+        mma16_ss(E2, L.p16a0, L.p16a1, b2);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) C[p][e] = combine3(E0[e], E1[e], E2[e]);
+    }
+}
+
+// paired n = 8 (U rows 0-7 | V rows 8-15): one B fragment (thread t < 2: U x = 4t..,
+// t >= 2: V x = 4(t-2)..; y = g) -> C[e]: e=0,1: U (i = g, j = 2t+e); e=2,3: V (i = g, j = 2t+e-2)
+template <int ES>
+__device__ __forceinline__ void dct8pair(const LaneConst &L, uint32_t blo, uint32_t bhi, int32_t (&C)[4])
+{
+    int32_t D1[4];
+    mma16_su(D1, L.t8a0, L.t8a1, blo);
+    if (ES == 2) {
+        int32_t Dh[4];
+        mma16_su(Dh, L.t8a0, L.t8a1, bhi);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D1[e] = (int32_t)((uint32_t)D1[e] + ((uint32_t)Dh[e] << 8));
+    }
+    uint32_t b0, b1, b2;
+    byte_planes(D1[0], D1[1], D1[2], D1[3], b0, b1, b2);
+    int32_t E0[4], E1[4], E2[4];
+    mma16_su(E0, L.p8a0, L.p8a1, b0);
+    mma16_su(E1, L.p8a0, L.p8a1, b1);
+    mma16_ss(E2, L.p8a0, L.p8a1, b2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) C[e] = combine3(E0[e], E1[e], E2[e]);
+}
+
+// ------------------------------------------------------------------ kernel
+struct FusedArgs {
+    int n_frames;
+    int width[3], height[3];
+    int cols, rows;
+    const double *W_all;
+    const int8_t *T_all;
+    Scratch s;
+    DumpPtrs dump;
+    uint64_t l2_policy_unused;
+};
+
+template <int W_, int BD_, int LP_, bool DUMP>
+__global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUtensorMap tmY,
+                                                    const __grid_constant__ CUtensorMap tmU,
+                                                    const __grid_constant__ CUtensorMap tmV, const FusedArgs a)
+{
+    using F = Fam<W_, BD_, LP_>;
+    constexpr int NY = F::NY, NC = F::NC, ES = F::ES, W = F::W, WC = F::WC;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + F::STAGES * F::STAGE);
+    uint64_t *empty = full + F::STAGES;
+    double *wtab = reinterpret_cast<double *>(empty + F::STAGES);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < F::STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], F::UNITS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (F::WTAB) {
+        // luma n = 32 weights in [slot][lane] order: slot = (mt*4 + r)*4 + e, lane (g, t):
+        // i = 16mt + g + 8(e>>1), j = 8r + 2t + (e&1)
+        const double *W32 = a.W_all + table_offset(32);
+        for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
+            const int slot = idx >> 5, ln = idx & 31, gg = ln >> 2, tt = ln & 3;
+            const int e = slot & 3, r = (slot >> 2) & 3, mt = slot >> 4;
+            const int i = 16 * mt + gg + 8 * (e >> 1), j = 8 * r + 2 * tt + (e & 1);
+            wtab[idx] = W32[i * 32 + j];
+        }
+    }
+    __syncthreads();
+
+    const int rows = a.rows, cols = a.cols;
+    const int strips = (cols + F::UNITS - 1) / F::UNITS;
+    const int64_t items = (int64_t)a.n_frames * rows;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (A1)
+        if (lane == 0) {
+            uint64_t policy;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmU)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
+            uint32_t seq = 0;
+            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+                const int f = (int)(it / rows), r = (int)(it - (int64_t)f * rows);
+                for (int s = 0; s < strips; ++s, ++seq) {
+                    const uint32_t st = seq % F::STAGES, use = seq / F::STAGES;
+                    if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
+                    uint8_t *base = smem + st * F::STAGE;
+                    mbar_expect_tx(&full[st], F::TX);
+#pragma unroll
+                    for (int b = 0; b < F::NBOX_Y; ++b)
+                        tma_load_3d(base + b * F::BOXB_Y, &tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * W,
+                                    r * W, f, policy);
+#pragma unroll
+                    for (int b = 0; b < F::NBOX_C; ++b) {
+                        tma_load_3d(base + F::ST_Y + b * F::BOXB_C, &tmU, &full[st],
+                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                        tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
+                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers
+    const int u = warp - 1;
+    const int g = lane >> 2, t = lane & 3;
+    LaneConst L;
+    build_lane_const(L, a.T_all, g, t, NY);
+    // per-lane scaled weights (A5): luma n = 16 positions (i = g + 8(e>>1), j = 8p + 2t + (e&1)),
+    // chroma positions of dct16 (NC = 16) or dct8pair (NC = 8)
+    double wl16[8], wc[NC == 16 ? 8 : 2];
+    {
+        const double *W16 = a.W_all + table_offset(16);
+        const double *W8 = a.W_all + table_offset(8);
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) wl16[p * 4 + e] = __ldg(W16 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1));
+        if (NC == 16) {
+#pragma unroll
+            for (int q = 0; q < (NC == 16 ? 8 : 2); ++q) wc[q] = wl16[q];
+        } else {
+#pragma unroll
+            for (int e = 0; e < (NC == 16 ? 8 : 2); ++e) wc[e] = __ldg(W8 + g * 8 + 2 * t + e);
+        }
+    }
+    const double invNY = 1.0 / NY, invNC = 1.0 / NC;
+
+    uint32_t seq = 0;
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int f = (int)(it / rows), r = (int)(it - (int64_t)f * rows);
+        const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
+        double hu = 0.0, hv = 0.0;                    // per-lane U/V texture partials (fixed order)
+        double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // lane 0
+        for (int s = 0; s < strips; ++s, ++seq) {
+            const uint32_t st = seq % F::STAGES, use = seq / F::STAGES;
+            mbar_wait(&full[st], use & 1);
+            const int c = s * F::UNITS + u;
+            if (c < cols) {
+                const uint8_t *base = smem + st * F::STAGE;
+                const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
+                const bool xpart = wvY < W;
+                const uint8_t *boxY = base + (u / F::UPB_Y) * F::BOXB_Y;
+                const uint8_t *boxU = base + F::ST_Y + (u / F::UPB_C) * F::BOXB_C;
+                const uint8_t *boxV = boxU + F::ST_C;
+                const int ubY = u % F::UPB_Y, ubC = u % F::UPB_C;
+                const int64_t k = (int64_t)r * cols + c;
+
+                // ---- luma
+                double hY = 0.0;
+                int32_t dcY = 0;
+                if (NY == 16) {
+                    uint32_t blo[2], bhi[2];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, xpart, blo[q], bhi[q]);
+                    int32_t C[2][4];
+                    dct16<ES>(L, blo, bhi, C);
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) hY = fma(wl16[p * 4 + e], abs_to_double(C[p][e]), hY);
+                    dcY = C[0][0];
+                    if (DUMP) {
+#pragma unroll
+                        for (int p = 0; p < 2; ++p)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                a.dump.coeffs[0][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+                    }
+                } else {
+                    // n = 32: pass 1 over 4 n-tiles (y = 8q + g), 2 m-tiles (j = 16mt + g (+8))
+                    int32_t D1[2][4][4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t l0, h0, l1, h1;
+                        load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, xpart, l0, h0);
+                        load4<F, 0>(boxY, ubY, 8 * q + g, 4 + t, hvY, wvY, xpart, l1, h1);
+#pragma unroll
+                        for (int mt = 0; mt < 2; ++mt) {
+                            mma32_su(D1[mt][q], L.t32[mt], l0, l1);
+                            if (ES == 2) {
+                                int32_t Dh[4];
+                                mma32_su(Dh, L.t32[mt], h0, h1);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    D1[mt][q][e] = (int32_t)((uint32_t)D1[mt][q][e] + ((uint32_t)Dh[e] << 8));
+                            }
+                        }
+                    }
+                    const double *wt = wtab + lane;
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr) {
+                        const int ms = rr >> 1, hf = rr & 1;
+                        uint32_t b0a, b1a, b2a, b0b, b1b, b2b;
+                        byte_planes(D1[ms][0][2 * hf], D1[ms][0][2 * hf + 1], D1[ms][1][2 * hf], D1[ms][1][2 * hf + 1],
+                                    b0a, b1a, b2a);
+                        byte_planes(D1[ms][2][2 * hf], D1[ms][2][2 * hf + 1], D1[ms][3][2 * hf], D1[ms][3][2 * hf + 1],
+                                    b0b, b1b, b2b);
+#pragma unroll
+                        for (int mt = 0; mt < 2; ++mt) {
+                            int32_t E0[4], E1[4], E2[4];
+                            mma32_su(E0, L.p32[mt], b0a, b0b);
+                            mma32_su(E1, L.p32[mt], b1a, b1b);
+                            mma32_ss(E2, L.p32[mt], b2a, b2b);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int32_t cc = combine3(E0[e], E1[e], E2[e]);
+                                hY = fma(wt[((mt * 4 + rr) * 4 + e) * 32], abs_to_double(cc), hY);
+                                if (mt == 0 && rr == 0 && e == 0) dcY = cc;
+                                if (DUMP)
+                                    a.dump.coeffs[0][k * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) hY += __shfl_xor_sync(0xffffffffu, hY, o);
+
+                // ---- chroma
+                int32_t dcU = 0, dcV = 0;
+                double huu = 0.0, hvv = 0.0;
+                if (NC == 8) {
+                    uint32_t blo, bhi;
+                    load4<F, 1>(t < 2 ? boxU : boxV, ubC, g, t & 1, hvC, wvC, xpart, blo, bhi);
+                    int32_t C[4];
+                    dct8pair<ES>(L, blo, bhi, C);
+                    huu = fma(wc[0], abs_to_double(C[0]), 0.0);
+                    huu = fma(wc[1], abs_to_double(C[1]), huu);
+                    hvv = fma(wc[0], abs_to_double(C[2]), 0.0);
+                    hvv = fma(wc[1], abs_to_double(C[3]), hvv);
+                    dcU = C[0];
+                    dcV = C[2];
+                    if (DUMP) {
+                        a.dump.coeffs[1][k * 64 + g * 8 + 2 * t] = C[0];
+                        a.dump.coeffs[1][k * 64 + g * 8 + 2 * t + 1] = C[1];
+                        a.dump.coeffs[2][k * 64 + g * 8 + 2 * t] = C[2];
+                        a.dump.coeffs[2][k * 64 + g * 8 + 2 * t + 1] = C[3];
+                    }
+                } else {
+#pragma unroll
+                    for (int pl = 1; pl <= 2; ++pl) {
+                        const uint8_t *box = pl == 1 ? boxU : boxV;
+                        uint32_t blo[2], bhi[2];
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC, 8 * q + g, t, hvC, wvC, xpart, blo[q], bhi[q]);
+                        int32_t C[2][4];
+                        dct16<ES>(L, blo, bhi, C);
+                        double hacc = 0.0;
+#pragma unroll
+                        for (int p = 0; p < 2; ++p)
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) hacc = fma(wc[p * 4 + e], abs_to_double(C[p][e]), hacc);
+                        if (pl == 1) { huu = hacc; dcU = C[0][0]; } else { hvv = hacc; dcV = C[0][0]; }
+                        if (DUMP) {
+#pragma unroll
+                            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    a.dump.coeffs[pl][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+                        }
+                    }
+                }
+                hu += huu;
+                hv += hvv;
+                if (DUMP) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        huu += __shfl_xor_sync(0xffffffffu, huu, o);
+                        hvv += __shfl_xor_sync(0xffffffffu, hvv, o);
+                    }
+                }
+                if (lane == 0) {
+                    // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
+                    const uint32_t sxY = (uint32_t)dcY >> 12, sxU = (uint32_t)dcU >> 12, sxV = (uint32_t)dcV >> 12;
+                    const double LY = sqrt((double)sxY * invNY), LU = sqrt((double)sxU * invNC),
+                                 LV = sqrt((double)sxV * invNC);
+                    sHY += hY;
+                    sLY += LY;
+                    sLU += LU;
+                    sLV += LV;
+                    a.s.HY[(int64_t)f * rows * cols + k] = hY;
+                    if (DUMP) {
+                        a.dump.sumx[0][k] = sxY;
+                        a.dump.sumx[1][k] = sxU;
+                        a.dump.sumx[2][k] = sxV;
+                        a.dump.H[0][k] = hY;
+                        a.dump.H[1][k] = huu;
+                        a.dump.H[2][k] = hvv;
+                        a.dump.L[0][k] = LY;
+                        a.dump.L[1][k] = LU;
+                        a.dump.L[2][k] = LV;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        // ---- item end: fixed-order partials of this warp's units (A7 inputs)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            hu += __shfl_xor_sync(0xffffffffu, hu, o);
+            hv += __shfl_xor_sync(0xffffffffu, hv, o);
+        }
+        if (lane == 0) {
+            const int64_t q = (int64_t)r * F::UNITS + u;
+            double *P0 = a.s.partial + (((int64_t)f * 3 + 0) * a.s.P + q) * 2;
+            double *P1 = a.s.partial + (((int64_t)f * 3 + 1) * a.s.P + q) * 2;
+            double *P2 = a.s.partial + (((int64_t)f * 3 + 2) * a.s.P + q) * 2;
+            P0[0] = sHY;
+            P0[1] = sLY;
+            P1[0] = hu;
+            P1[1] = sLU;
+            P2[0] = hv;
+            P2[1] = sLV;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+inline bool fused_supported(int w, int lowpass, bool grids_equal)
+{
+    return grids_equal && (w == 32 || (w == 16 && !lowpass));
+}
+inline int fused_partials_per_row() { return 4; }
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode()
+{
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+
+inline bool make_map(CUtensorMap *m, const PlaneDesc &P, int n_frames, int es, int inner_bytes, int box_rows)
+{
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)P.width, (cuuint64_t)P.height, (cuuint64_t)n_frames};
+    cuuint64_t strides[2] = {(cuuint64_t)P.pitch, (cuuint64_t)(P.fstride > 0 ? P.fstride : P.pitch * P.height)};
+    cuuint32_t box[3] = {(cuuint32_t)(inner_bytes / es), (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMapSwizzle sw = inner_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : inner_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = enc(m, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                     const_cast<uint8_t *>(P.base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int W, int BD, int LP>
+inline cudaError_t prepare_one()
+{
+    using F = Fam<W, BD, LP>;
+    cudaError_t e = cudaFuncSetAttribute(fused_kernel<W, BD, LP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         F::SMEM);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(fused_kernel<W, BD, LP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM);
+    return e;
+}
+
+inline cudaError_t fused_prepare(int bd, int lowpass, int w)
+{
+    if (w == 32 && lowpass) return bd == 8 ? prepare_one<32, 8, 1>() : prepare_one<32, 10, 1>();
+    if (w == 32) return bd == 8 ? prepare_one<32, 8, 0>() : prepare_one<32, 10, 0>();
+    return bd == 8 ? prepare_one<16, 8, 0>() : prepare_one<16, 10, 0>();
+}
+
+template <int W, int BD, int LP>
+inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const double *Wt, const Scratch &s,
+                      const DumpPtrs &dp, int sm_count, cudaStream_t st)
+{
+    using F = Fam<W, BD, LP>;
+    CUtensorMap mY, mU, mV;
+    if (!make_map(&mY, pl.p[0], n_frames, F::ES, F::IB_Y, W) || !make_map(&mU, pl.p[1], n_frames, F::ES, F::IB_C, W / 2) ||
+        !make_map(&mV, pl.p[2], n_frames, F::ES, F::IB_C, W / 2))
+        return -2;
+    FusedArgs a;
+    a.n_frames = n_frames;
+    for (int p = 0; p < 3; ++p) {
+        a.width[p] = pl.p[p].width;
+        a.height[p] = pl.p[p].height;
+    }
+    a.cols = pl.p[0].cols;
+    a.rows = pl.p[0].rows;
+    a.W_all = Wt;
+    a.T_all = T;
+    a.s = s;
+    a.dump = dp;
+    a.l2_policy_unused = 0;
+    const bool dump = dp.coeffs[0] != nullptr;
+    auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 160, F::SMEM) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int64_t items = (int64_t)n_frames * a.rows;
+    int64_t grid = (int64_t)sm_count * per_sm;
+    if (grid > items) grid = items;
+    kern<<<(unsigned)grid, 160, F::SMEM, st>>>(mY, mU, mV, a);
+    return 0;
+}
+
+// Returns 0 on launch, -1 on a CUDA launch failure (see cudaGetLastError), -2 if a
+// tensor map could not be encoded.
+inline int launch_fused(const Planes3 &pl, int n_frames, int bd, int lowpass, const int8_t *T, const double *Wt,
+                        const Scratch &s, const DumpPtrs &dp, int sm_count, cudaStream_t st)
+{
+    const int w = pl.p[0].w;
+    if (w == 32 && lowpass)
+        return bd == 8 ? launch_one<32, 8, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st)
+                       : launch_one<32, 10, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+    if (w == 32)
+        return bd == 8 ? launch_one<32, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
+                       : launch_one<32, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+    return bd == 8 ? launch_one<16, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
+                   : launch_one<16, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
 }
 
 }  // namespace vca

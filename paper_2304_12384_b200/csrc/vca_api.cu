@@ -183,8 +183,8 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         VCA_CK(ctx, cudaEventRecord(ev.e[0], st));
     }
     if (ctx->path == VCA_PATH_FUSED_MMA) {
-        int rc = launch_fused(pl, n_frames, ctx->bd, ctx->lowpass, ctx->d_T, ctx->d_W, s, dp, ctx->sm_count, st);
-        if (rc == -1) return fail_cuda(ctx, cudaGetLastError() == cudaSuccess ? cudaErrorUnknown : cudaErrorUnknown);
+        const int rc = launch_fused(pl, n_frames, ctx->bd, ctx->lowpass, ctx->d_T, ctx->d_W, s, dp, ctx->sm_count, st);
+        if (rc == -2) return VCA_ERR_INVALID_ARG;  // tensor map not encodable for these strides
     } else {
         const int64_t tasks = (int64_t)n_frames * (ctx->geo[0].count + ctx->geo[1].count + ctx->geo[2].count);
         int64_t blocks = (tasks + kGenericWarps - 1) / kGenericWarps;
