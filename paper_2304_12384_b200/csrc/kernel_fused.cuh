@@ -151,9 +151,12 @@ struct Fam {
     static constexpr int ST_Y = NBOX_Y * BOXB_Y, ST_C = NBOX_C * BOXB_C;
     static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
     static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
-    static constexpr int STAGES = (49152 / STAGE) < 4 ? 4 : (49152 / STAGE > 16 ? 16 : 49152 / STAGE);
+    static constexpr int RING = 36864;  // ring bytes per CTA (several CTAs per SM)
+    static constexpr int STAGES = (RING / STAGE) < 4 ? 4 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);               // luma weights from smem (32 per lane)
-    static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0);
+    static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;  // per consumer warp
+    static constexpr int SMEM =
+        1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + UNITS * STASH;
     static_assert(NC == NY / 2, "chroma DCT is half the luma DCT");
     static_assert(IB_Y == 32 || IB_Y == 64 || IB_Y == 128, "swizzle span");
     static_assert(IB_C == 32 || IB_C == 64 || IB_C == 128, "swizzle span");
@@ -166,12 +169,43 @@ __device__ __forceinline__ uint32_t swz(uint32_t off)
     return off ^ (((off >> 7) & m) << 4);
 }
 
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a)
+{
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
 // One sample of a unit in a swizzled box (row, column within the unit), 10-bit clamp
 template <int ES, int IB>
-__device__ __forceinline__ int box_sample(const uint8_t *box, int ub0, int row, int xs)
+__device__ __forceinline__ int box_sample(uint32_t box, int ub0, int row, int xs)
 {
-    if (ES == 1) return box[swz<IB>(row * IB + ub0 + xs)];
-    const int v = *reinterpret_cast<const uint16_t *>(box + swz<IB>(row * IB + ub0 + 2 * xs));
+    if (ES == 1) return (int)lds_u8(box + swz<IB>(row * IB + ub0 + xs));
+    const int v = (int)lds_u16(box + swz<IB>(row * IB + ub0 + 2 * xs));
     return v < 1023 ? v : 1023;
 }
 
@@ -193,7 +227,7 @@ __device__ __forceinline__ uint32_t pair_sum16(uint32_t v)
 // byte planes lo (and hi for 10-bit).  hv/wv: valid rows/columns of the unit in
 // source samples (edge replication by clamping); xpart: wv < block width.
 template <class F, int PL>
-__device__ __forceinline__ void load4(const uint8_t *box, int ub, int y, int xg, int hv, int wv, bool xpart,
+__device__ __forceinline__ void load4(uint32_t box, int ub, int y, int xg, int hv, int wv, bool xpart,
                                       uint32_t &lo, uint32_t &hi)
 {
     constexpr int IB = PL == 0 ? F::IB_Y : F::IB_C;
@@ -204,10 +238,10 @@ __device__ __forceinline__ void load4(const uint8_t *box, int ub, int y, int xg,
         if (!F::LP) {
             const int row = min(y, hv - 1);
             if (ES == 1) {
-                lo = *reinterpret_cast<const uint32_t *>(box + swz<IB>(row * IB + ub0 + 4 * xg));
+                lo = lds32(box + swz<IB>(row * IB + ub0 + 4 * xg));
                 hi = 0;
             } else {
-                uint2 v = *reinterpret_cast<const uint2 *>(box + swz<IB>(row * IB + ub0 + 8 * xg));
+                uint2 v = lds64(box + swz<IB>(row * IB + ub0 + 8 * xg));
                 v.x = __vminu2(v.x, 0x03FF03FFu);
                 v.y = __vminu2(v.y, 0x03FF03FFu);
                 lo = __byte_perm(v.x, v.y, 0x6420);
@@ -216,13 +250,13 @@ __device__ __forceinline__ void load4(const uint8_t *box, int ub, int y, int xg,
         } else {
             const int r0 = min(2 * y, hv - 1), r1 = min(2 * y + 1, hv - 1);
             if (ES == 1) {
-                const uint2 a = *reinterpret_cast<const uint2 *>(box + swz<IB>(r0 * IB + ub0 + 8 * xg));
-                const uint2 b = *reinterpret_cast<const uint2 *>(box + swz<IB>(r1 * IB + ub0 + 8 * xg));
+                const uint2 a = lds64(box + swz<IB>(r0 * IB + ub0 + 8 * xg));
+                const uint2 b = lds64(box + swz<IB>(r1 * IB + ub0 + 8 * xg));
                 lo = ds8(a, b);
                 hi = 0;
             } else {
-                uint4 a = *reinterpret_cast<const uint4 *>(box + swz<IB>(r0 * IB + ub0 + 16 * xg));
-                uint4 b = *reinterpret_cast<const uint4 *>(box + swz<IB>(r1 * IB + ub0 + 16 * xg));
+                uint4 a = lds128(box + swz<IB>(r0 * IB + ub0 + 16 * xg));
+                uint4 b = lds128(box + swz<IB>(r1 * IB + ub0 + 16 * xg));
                 const uint32_t C10 = 0x03FF03FFu;
                 const uint32_t d0 = (pair_sum16(__vminu2(a.x, C10)) + pair_sum16(__vminu2(b.x, C10)) + 2) >> 2;
                 const uint32_t d1 = (pair_sum16(__vminu2(a.y, C10)) + pair_sum16(__vminu2(b.y, C10)) + 2) >> 2;
@@ -403,6 +437,8 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + F::STAGES * F::STAGE);
     uint64_t *empty = full + F::STAGES;
     double *wtab = reinterpret_cast<double *>(empty + F::STAGES);
+    // per consumer warp: hst[32 slots][9] (8 row-group partials, padded) + sxs[32][4] DC sums
+    uint8_t *stash = reinterpret_cast<uint8_t *>(wtab + (F::WTAB ? 32 * 32 : 0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -427,7 +463,7 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
 
     const int rows = a.rows, cols = a.cols;
     const int strips = (cols + F::UNITS - 1) / F::UNITS;
-    const int64_t items = (int64_t)a.n_frames * rows;
+    const int items = a.n_frames * rows;  // < 2^31 (checked on the host)
 
     if (warp == 0) {
         // ---------------- TMA producer (A1)
@@ -438,8 +474,8 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmU)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
             uint32_t seq = 0;
-            for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-                const int f = (int)(it / rows), r = (int)(it - (int64_t)f * rows);
+            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+                const int f = it / rows, r = it - f * rows;
                 for (int s = 0; s < strips; ++s, ++seq) {
                     const uint32_t st = seq % F::STAGES, use = seq / F::STAGES;
                     if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
@@ -465,6 +501,8 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
     // ---------------- consumers
     const int u = warp - 1;
     const int g = lane >> 2, t = lane & 3;
+    double *hst = reinterpret_cast<double *>(stash + u * F::STASH);
+    uint32_t *sxs = reinterpret_cast<uint32_t *>(stash + u * F::STASH + 32 * 9 * 8);
     LaneConst L;
     build_lane_const(L, a.T_all, g, t, NY);
     // per-lane scaled weights (A5): luma n = 16 positions (i = g + 8(e>>1), j = 8p + 2t + (e&1)),
@@ -488,11 +526,11 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
     const double invNY = 1.0 / NY, invNC = 1.0 / NC;
 
     uint32_t seq = 0;
-    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int f = (int)(it / rows), r = (int)(it - (int64_t)f * rows);
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        const int f = it / rows, r = it - f * rows;
         const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
         double hu = 0.0, hv = 0.0;                    // per-lane U/V texture partials (fixed order)
-        double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // lane 0
+        double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // identical in all lanes
         for (int s = 0; s < strips; ++s, ++seq) {
             const uint32_t st = seq % F::STAGES, use = seq / F::STAGES;
             mbar_wait(&full[st], use & 1);
@@ -501,9 +539,9 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                 const uint8_t *base = smem + st * F::STAGE;
                 const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
                 const bool xpart = wvY < W;
-                const uint8_t *boxY = base + (u / F::UPB_Y) * F::BOXB_Y;
-                const uint8_t *boxU = base + F::ST_Y + (u / F::UPB_C) * F::BOXB_C;
-                const uint8_t *boxV = boxU + F::ST_C;
+                const uint32_t boxY = smem_u32(base) + (u / F::UPB_Y) * F::BOXB_Y;
+                const uint32_t boxU = smem_u32(base) + F::ST_Y + (u / F::UPB_C) * F::BOXB_C;
+                const uint32_t boxV = boxU + F::ST_C;
                 const int ubY = u % F::UPB_Y, ubC = u % F::UPB_C;
                 const int64_t k = (int64_t)r * cols + c;
 
@@ -575,8 +613,9 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                         }
                     }
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) hY += __shfl_xor_sync(0xffffffffu, hY, o);
+                // reduce over the 4 lanes of a row group: lanes t == 0 hold the partial of rows g (+8, ...)
+                hY += __shfl_xor_sync(0xffffffffu, hY, 1);
+                hY += __shfl_xor_sync(0xffffffffu, hY, 2);
 
                 // ---- chroma
                 int32_t dcU = 0, dcV = 0;
@@ -601,7 +640,7 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                 } else {
 #pragma unroll
                     for (int pl = 1; pl <= 2; ++pl) {
-                        const uint8_t *box = pl == 1 ? boxU : boxV;
+                        const uint32_t box = pl == 1 ? boxU : boxV;
                         uint32_t blo[2], bhi[2];
 #pragma unroll
                         for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC, 8 * q + g, t, hvC, wvC, xpart, blo[q], bhi[q]);
@@ -624,35 +663,65 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                 }
                 hu += huu;
                 hv += hvv;
+                // stash: per-unit luma row-group partials and DC sums, reduced 32 units at a time
+                const int slot = s & 31;
+                if (t == 0) hst[slot * 9 + g] = hY;
+                if (lane == 0) {
+                    // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
+                    sxs[slot * 4 + 0] = (uint32_t)dcY >> 12;
+                    sxs[slot * 4 + 1] = (uint32_t)dcU >> 12;
+                    sxs[slot * 4 + 2] = (uint32_t)dcV >> 12;
+                }
                 if (DUMP) {
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) hY += __shfl_xor_sync(0xffffffffu, hY, o);
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
                         huu += __shfl_xor_sync(0xffffffffu, huu, o);
                         hvv += __shfl_xor_sync(0xffffffffu, hvv, o);
                     }
-                }
-                if (lane == 0) {
-                    // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
-                    const uint32_t sxY = (uint32_t)dcY >> 12, sxU = (uint32_t)dcU >> 12, sxV = (uint32_t)dcV >> 12;
-                    const double LY = sqrt((double)sxY * invNY), LU = sqrt((double)sxU * invNC),
-                                 LV = sqrt((double)sxV * invNC);
-                    sHY += hY;
-                    sLY += LY;
-                    sLU += LU;
-                    sLV += LV;
-                    a.s.HY[(int64_t)f * rows * cols + k] = hY;
-                    if (DUMP) {
+                    if (lane == 0) {
+                        const uint32_t sxY = (uint32_t)dcY >> 12, sxU = (uint32_t)dcU >> 12, sxV = (uint32_t)dcV >> 12;
                         a.dump.sumx[0][k] = sxY;
                         a.dump.sumx[1][k] = sxU;
                         a.dump.sumx[2][k] = sxV;
                         a.dump.H[0][k] = hY;
                         a.dump.H[1][k] = huu;
                         a.dump.H[2][k] = hvv;
-                        a.dump.L[0][k] = LY;
-                        a.dump.L[1][k] = LU;
-                        a.dump.L[2][k] = LV;
+                        a.dump.L[0][k] = sqrt((double)sxY * invNY);
+                        a.dump.L[1][k] = sqrt((double)sxU * invNC);
+                        a.dump.L[2][k] = sqrt((double)sxV * invNC);
                     }
                 }
+            }
+            if ((s & 31) == 31 || s == strips - 1) {
+                // flush: lane l finishes unit slot l -- H_Y (fixed order over the 8 row
+                // groups), its L terms (A6), the per-block H_Y store (A5, needed for h);
+                // then a fixed xor tree over lanes into the running item sums.
+                __syncwarp();
+                const int slot = s & 31;
+                const int cl = (s - slot + lane) * F::UNITS + u;
+                double Hl = 0.0, LYl = 0.0, LUl = 0.0, LVl = 0.0;
+                if (lane <= slot && cl < cols) {
+#pragma unroll
+                    for (int gg = 0; gg < 8; ++gg) Hl += hst[lane * 9 + gg];
+                    LYl = sqrt((double)sxs[lane * 4 + 0] * invNY);
+                    LUl = sqrt((double)sxs[lane * 4 + 1] * invNC);
+                    LVl = sqrt((double)sxs[lane * 4 + 2] * invNC);
+                    a.s.HY[(int64_t)f * rows * cols + (int64_t)r * cols + cl] = Hl;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    Hl += __shfl_xor_sync(0xffffffffu, Hl, o);
+                    LYl += __shfl_xor_sync(0xffffffffu, LYl, o);
+                    LUl += __shfl_xor_sync(0xffffffffu, LUl, o);
+                    LVl += __shfl_xor_sync(0xffffffffu, LVl, o);
+                }
+                sHY += Hl;
+                sLY += LYl;
+                sLU += LUl;
+                sLV += LVl;
+                __syncwarp();
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
@@ -765,6 +834,7 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 160, F::SMEM) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     const int64_t items = (int64_t)n_frames * a.rows;
+    if (items > 0x7fffffff) return -2;
     int64_t grid = (int64_t)sm_count * per_sm;
     if (grid > items) grid = items;
     kern<<<(unsigned)grid, 160, F::SMEM, st>>>(mY, mU, mV, a);
