@@ -57,14 +57,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+// Blocking wait on an mbarrier phase; the suspend-time hint lets the warp sleep
+// in try_wait until the phase completes instead of spinning on issue slots.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
     asm volatile(
         "{\n\t.reg .pred P;\n"
         "VCA_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-        "@!P bra VCA_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+        "@!P bra VCA_WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity), "r"(1000000)
         : "memory");
 }
 
@@ -210,12 +212,15 @@ __device__ __forceinline__ int box_sample(uint32_t box, int ub0, int row, int xs
 }
 
 // 8-bit 2x2 low-pass of two source rows of 8 bytes -> 4 packed outputs, (s+2)>>2 (R-5)
+// Each 32-bit word holds 4 samples; even/odd samples go to 16-bit lanes (LOP3 /
+// PRMT), the 2x2 sums (<= 1020) plus 2 are formed per lane, and the final PRMT
+// picks byte 0 of each lane after >> 2 (s >> 2 <= 255, so no masking is needed).
 __device__ __forceinline__ uint32_t ds8(uint2 a, uint2 b)
 {
     const uint32_t M = 0x00FF00FFu;
-    const uint32_t sl = (a.x & M) + ((a.x >> 8) & M) + (b.x & M) + ((b.x >> 8) & M) + 0x00020002u;
-    const uint32_t sh = (a.y & M) + ((a.y >> 8) & M) + (b.y & M) + ((b.y >> 8) & M) + 0x00020002u;
-    return __byte_perm((sl >> 2) & M, (sh >> 2) & M, 0x6420);
+    const uint32_t sl = (a.x & M) + __byte_perm(a.x, 0u, 0x4341) + (b.x & M) + __byte_perm(b.x, 0u, 0x4341) + 0x00020002u;
+    const uint32_t sh = (a.y & M) + __byte_perm(a.y, 0u, 0x4341) + (b.y & M) + __byte_perm(b.y, 0u, 0x4341) + 0x00020002u;
+    return __byte_perm(sl >> 2, sh >> 2, 0x6420);
 }
 
 __device__ __forceinline__ uint32_t pair_sum16(uint32_t v)
@@ -413,6 +418,8 @@ __device__ __forceinline__ void dct8pair(const LaneConst &L, uint32_t blo, uint3
     for (int e = 0; e < 4; ++e) C[e] = combine3(E0[e], E1[e], E2[e]);
 }
 
+
+
 // ------------------------------------------------------------------ kernel
 struct FusedArgs {
     int n_frames;
@@ -424,6 +431,171 @@ struct FusedArgs {
     DumpPtrs dump;
     uint64_t l2_policy_unused;
 };
+
+template <class F>
+struct UnitCtx {
+    static constexpr int NWC = F::NC == 16 ? 8 : 2;
+    LaneConst L;
+    double wl16[8];     // luma n = 16 weights at this lane's 8 positions
+    double wc[NWC];     // chroma weights at this lane's positions
+    const double *wtab; // luma n = 32 weights in smem, [slot][lane] + lane
+    int g, t;
+};
+
+struct UnitOut {
+    double hY;          // luma texture partial, summed over the 4 lanes of row group g
+    double hu, hv;      // this lane's U / V texture partials
+    int32_t dcY, dcU, dcV;  // C_00 (mod 2^32) in lane 0
+};
+
+// A2-A6 for one unit (Y block + U, V blocks): swizzled smem -> registers ->
+// exact integer DCT on the tensor cores -> FP64 weighted |C| partials.
+template <class F, bool XPART, bool DUMP>
+__device__ __forceinline__ void process_unit(const UnitCtx<F> &U, const FusedArgs &a, uint32_t boxY, uint32_t boxU,
+                                             int ubY, int ubC, int hvY, int hvC, int wvY, int wvC, int64_t k,
+                                             UnitOut &o)
+{
+    constexpr int NY = F::NY, NC = F::NC, ES = F::ES;
+    const int g = U.g, t = U.t;
+    const LaneConst &L = U.L;
+    const uint32_t boxV = boxU + F::ST_C;
+    double hY = 0.0;
+    if (NY == 16) {
+        uint32_t blo[2], bhi[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, XPART, blo[q], bhi[q]);
+        int32_t C[2][4];
+        dct16<ES>(L, blo, bhi, C);
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hY = fma(U.wl16[p * 4 + e], abs_to_double(C[p][e]), hY);
+        o.dcY = C[0][0];
+        if (DUMP) {
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    a.dump.coeffs[0][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+        }
+    } else {
+        // n = 32: pass 1 over 4 n-tiles (y = 8q + g), 2 m-tiles (j = 16mt + g (+8))
+        int32_t D1[2][4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t l0, h0, l1, h1;
+            load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, XPART, l0, h0);
+            load4<F, 0>(boxY, ubY, 8 * q + g, 4 + t, hvY, wvY, XPART, l1, h1);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                mma32_su(D1[mt][q], L.t32[mt], l0, l1);
+                if (ES == 2) {
+                    int32_t Dh[4];
+                    mma32_su(Dh, L.t32[mt], h0, h1);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) D1[mt][q][e] = (int32_t)((uint32_t)D1[mt][q][e] + ((uint32_t)Dh[e] << 8));
+                }
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+            const int ms = rr >> 1, hf = rr & 1;
+            uint32_t b0a, b1a, b2a, b0b, b1b, b2b;
+            byte_planes(D1[ms][0][2 * hf], D1[ms][0][2 * hf + 1], D1[ms][1][2 * hf], D1[ms][1][2 * hf + 1], b0a, b1a,
+                        b2a);
+            byte_planes(D1[ms][2][2 * hf], D1[ms][2][2 * hf + 1], D1[ms][3][2 * hf], D1[ms][3][2 * hf + 1], b0b, b1b,
+                        b2b);
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                int32_t E0[4], E1[4], E2[4];
+                mma32_su(E0, L.p32[mt], b0a, b0b);
+                mma32_su(E1, L.p32[mt], b1a, b1b);
+                mma32_ss(E2, L.p32[mt], b2a, b2b);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int32_t cc = combine3(E0[e], E1[e], E2[e]);
+                    hY = fma(U.wtab[((mt * 4 + rr) * 4 + e) * 32], abs_to_double(cc), hY);
+                    if (mt == 0 && rr == 0 && e == 0) o.dcY = cc;
+                    if (DUMP)
+                        a.dump.coeffs[0][k * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
+                }
+            }
+        }
+    }
+    // reduce over the 4 lanes of a row group: lanes t == 0 hold the partial of rows g (+8, ...)
+    hY += __shfl_xor_sync(0xffffffffu, hY, 1);
+    hY += __shfl_xor_sync(0xffffffffu, hY, 2);
+    o.hY = hY;
+
+    // ---- chroma
+    if (NC == 8) {
+        uint32_t blo, bhi;
+        load4<F, 1>(t < 2 ? boxU : boxV, ubC, g, t & 1, hvC, wvC, XPART, blo, bhi);
+        int32_t C[4];
+        dct8pair<ES>(L, blo, bhi, C);
+        o.hu = fma(U.wc[1], abs_to_double(C[1]), U.wc[0] * abs_to_double(C[0]));
+        o.hv = fma(U.wc[1], abs_to_double(C[3]), U.wc[0] * abs_to_double(C[2]));
+        o.dcU = C[0];
+        o.dcV = C[2];
+        if (DUMP) {
+            a.dump.coeffs[1][k * 64 + g * 8 + 2 * t] = C[0];
+            a.dump.coeffs[1][k * 64 + g * 8 + 2 * t + 1] = C[1];
+            a.dump.coeffs[2][k * 64 + g * 8 + 2 * t] = C[2];
+            a.dump.coeffs[2][k * 64 + g * 8 + 2 * t + 1] = C[3];
+        }
+    } else {
+#pragma unroll
+        for (int pl = 1; pl <= 2; ++pl) {
+            const uint32_t box = pl == 1 ? boxU : boxV;
+            uint32_t blo[2], bhi[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC, 8 * q + g, t, hvC, wvC, XPART, blo[q], bhi[q]);
+            int32_t C[2][4];
+            dct16<ES>(L, blo, bhi, C);
+            double hacc = 0.0;
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) hacc = fma(U.wc[p * 4 + e], abs_to_double(C[p][e]), hacc);
+            if (pl == 1) {
+                o.hu = hacc;
+                o.dcU = C[0][0];
+            } else {
+                o.hv = hacc;
+                o.dcV = C[0][0];
+            }
+            if (DUMP) {
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        a.dump.coeffs[pl][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+            }
+        }
+    }
+    if (DUMP) {
+        double hy = hY, hu = o.hu, hv = o.hv;
+#pragma unroll
+        for (int s = 4; s < 32; s <<= 1) hy += __shfl_xor_sync(0xffffffffu, hy, s);
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            hu += __shfl_xor_sync(0xffffffffu, hu, s);
+            hv += __shfl_xor_sync(0xffffffffu, hv, s);
+        }
+        if (g == 0 && t == 0) {
+            const uint32_t sxY = (uint32_t)o.dcY >> 12, sxU = (uint32_t)o.dcU >> 12, sxV = (uint32_t)o.dcV >> 12;
+            a.dump.sumx[0][k] = sxY;
+            a.dump.sumx[1][k] = sxU;
+            a.dump.sumx[2][k] = sxV;
+            a.dump.H[0][k] = hy;
+            a.dump.H[1][k] = hu;
+            a.dump.H[2][k] = hv;
+            a.dump.L[0][k] = sqrt((double)sxY * (1.0 / NY));
+            a.dump.L[1][k] = sqrt((double)sxU * (1.0 / NC));
+            a.dump.L[2][k] = sqrt((double)sxV * (1.0 / NC));
+        }
+    }
+}
 
 template <int W_, int BD_, int LP_, bool DUMP>
 __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUtensorMap tmY,
@@ -473,12 +645,12 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmU)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
-            uint32_t seq = 0;
+            uint32_t st = 0, phase = 0;
+            bool first_pass = true;
             for (int it = blockIdx.x; it < items; it += gridDim.x) {
                 const int f = it / rows, r = it - f * rows;
-                for (int s = 0; s < strips; ++s, ++seq) {
-                    const uint32_t st = seq % F::STAGES, use = seq / F::STAGES;
-                    if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
+                for (int s = 0; s < strips; ++s) {
+                    if (!first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
                     uint8_t *base = smem + st * F::STAGE;
                     mbar_expect_tx(&full[st], F::TX);
 #pragma unroll
@@ -492,6 +664,11 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                         tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
                                     (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
                     }
+                    if (++st == F::STAGES) {
+                        st = 0;
+                        phase ^= 1;
+                        first_pass = false;
+                    }
                 }
             }
         }
@@ -503,203 +680,74 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
     const int g = lane >> 2, t = lane & 3;
     double *hst = reinterpret_cast<double *>(stash + u * F::STASH);
     uint32_t *sxs = reinterpret_cast<uint32_t *>(stash + u * F::STASH + 32 * 9 * 8);
-    LaneConst L;
-    build_lane_const(L, a.T_all, g, t, NY);
+    UnitCtx<F> U;
+    build_lane_const(U.L, a.T_all, g, t, NY);
     // per-lane scaled weights (A5): luma n = 16 positions (i = g + 8(e>>1), j = 8p + 2t + (e&1)),
     // chroma positions of dct16 (NC = 16) or dct8pair (NC = 8)
-    double wl16[8], wc[NC == 16 ? 8 : 2];
     {
         const double *W16 = a.W_all + table_offset(16);
         const double *W8 = a.W_all + table_offset(8);
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) wl16[p * 4 + e] = __ldg(W16 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1));
-        if (NC == 16) {
+            for (int e = 0; e < 4; ++e)
+                U.wl16[p * 4 + e] = __ldg(W16 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1));
 #pragma unroll
-            for (int q = 0; q < (NC == 16 ? 8 : 2); ++q) wc[q] = wl16[q];
-        } else {
-#pragma unroll
-            for (int e = 0; e < (NC == 16 ? 8 : 2); ++e) wc[e] = __ldg(W8 + g * 8 + 2 * t + e);
-        }
+        for (int e = 0; e < UnitCtx<F>::NWC; ++e)
+            U.wc[e] = NC == 16 ? U.wl16[e] : __ldg(W8 + g * 8 + 2 * t + e);
     }
+    U.wtab = wtab + lane;
+    U.g = g;
+    U.t = t;
     const double invNY = 1.0 / NY, invNC = 1.0 / NC;
+    const uint32_t smem0 = smem_u32(smem);
+    const uint32_t full0 = smem_u32(full);
+    const int64_t CY = (int64_t)rows * cols;
 
-    uint32_t seq = 0;
+    uint32_t st = 0, phase = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int f = it / rows, r = it - f * rows;
         const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
-        double hu = 0.0, hv = 0.0;                    // per-lane U/V texture partials (fixed order)
+        double hu = 0.0, hv = 0.0;                          // per-lane U/V texture partials (fixed order)
         double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // identical in all lanes
-        for (int s = 0; s < strips; ++s, ++seq) {
-            const uint32_t st = seq % F::STAGES, use = seq / F::STAGES;
-            mbar_wait(&full[st], use & 1);
+        double *HYrow = a.s.HY + (int64_t)f * CY + (int64_t)r * cols;
+        for (int s = 0; s < strips; ++s) {
+            mbar_wait(full0 + 8 * st, phase);
             const int c = s * F::UNITS + u;
+            const int slot = s & 31;
             if (c < cols) {
-                const uint8_t *base = smem + st * F::STAGE;
+                const uint32_t base = smem0 + st * F::STAGE;
                 const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
-                const bool xpart = wvY < W;
-                const uint32_t boxY = smem_u32(base) + (u / F::UPB_Y) * F::BOXB_Y;
-                const uint32_t boxU = smem_u32(base) + F::ST_Y + (u / F::UPB_C) * F::BOXB_C;
-                const uint32_t boxV = boxU + F::ST_C;
-                const int ubY = u % F::UPB_Y, ubC = u % F::UPB_C;
-                const int64_t k = (int64_t)r * cols + c;
-
-                // ---- luma
-                double hY = 0.0;
-                int32_t dcY = 0;
-                if (NY == 16) {
-                    uint32_t blo[2], bhi[2];
-#pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, xpart, blo[q], bhi[q]);
-                    int32_t C[2][4];
-                    dct16<ES>(L, blo, bhi, C);
-#pragma unroll
-                    for (int p = 0; p < 2; ++p)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) hY = fma(wl16[p * 4 + e], abs_to_double(C[p][e]), hY);
-                    dcY = C[0][0];
-                    if (DUMP) {
-#pragma unroll
-                        for (int p = 0; p < 2; ++p)
-#pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                a.dump.coeffs[0][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
-                    }
-                } else {
-                    // n = 32: pass 1 over 4 n-tiles (y = 8q + g), 2 m-tiles (j = 16mt + g (+8))
-                    int32_t D1[2][4][4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint32_t l0, h0, l1, h1;
-                        load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, xpart, l0, h0);
-                        load4<F, 0>(boxY, ubY, 8 * q + g, 4 + t, hvY, wvY, xpart, l1, h1);
-#pragma unroll
-                        for (int mt = 0; mt < 2; ++mt) {
-                            mma32_su(D1[mt][q], L.t32[mt], l0, l1);
-                            if (ES == 2) {
-                                int32_t Dh[4];
-                                mma32_su(Dh, L.t32[mt], h0, h1);
-#pragma unroll
-                                for (int e = 0; e < 4; ++e)
-                                    D1[mt][q][e] = (int32_t)((uint32_t)D1[mt][q][e] + ((uint32_t)Dh[e] << 8));
-                            }
-                        }
-                    }
-                    const double *wt = wtab + lane;
-#pragma unroll
-                    for (int rr = 0; rr < 4; ++rr) {
-                        const int ms = rr >> 1, hf = rr & 1;
-                        uint32_t b0a, b1a, b2a, b0b, b1b, b2b;
-                        byte_planes(D1[ms][0][2 * hf], D1[ms][0][2 * hf + 1], D1[ms][1][2 * hf], D1[ms][1][2 * hf + 1],
-                                    b0a, b1a, b2a);
-                        byte_planes(D1[ms][2][2 * hf], D1[ms][2][2 * hf + 1], D1[ms][3][2 * hf], D1[ms][3][2 * hf + 1],
-                                    b0b, b1b, b2b);
-#pragma unroll
-                        for (int mt = 0; mt < 2; ++mt) {
-                            int32_t E0[4], E1[4], E2[4];
-                            mma32_su(E0, L.p32[mt], b0a, b0b);
-                            mma32_su(E1, L.p32[mt], b1a, b1b);
-                            mma32_ss(E2, L.p32[mt], b2a, b2b);
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const int32_t cc = combine3(E0[e], E1[e], E2[e]);
-                                hY = fma(wt[((mt * 4 + rr) * 4 + e) * 32], abs_to_double(cc), hY);
-                                if (mt == 0 && rr == 0 && e == 0) dcY = cc;
-                                if (DUMP)
-                                    a.dump.coeffs[0][k * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
-                            }
-                        }
-                    }
-                }
-                // reduce over the 4 lanes of a row group: lanes t == 0 hold the partial of rows g (+8, ...)
-                hY += __shfl_xor_sync(0xffffffffu, hY, 1);
-                hY += __shfl_xor_sync(0xffffffffu, hY, 2);
-
-                // ---- chroma
-                int32_t dcU = 0, dcV = 0;
-                double huu = 0.0, hvv = 0.0;
-                if (NC == 8) {
-                    uint32_t blo, bhi;
-                    load4<F, 1>(t < 2 ? boxU : boxV, ubC, g, t & 1, hvC, wvC, xpart, blo, bhi);
-                    int32_t C[4];
-                    dct8pair<ES>(L, blo, bhi, C);
-                    huu = fma(wc[0], abs_to_double(C[0]), 0.0);
-                    huu = fma(wc[1], abs_to_double(C[1]), huu);
-                    hvv = fma(wc[0], abs_to_double(C[2]), 0.0);
-                    hvv = fma(wc[1], abs_to_double(C[3]), hvv);
-                    dcU = C[0];
-                    dcV = C[2];
-                    if (DUMP) {
-                        a.dump.coeffs[1][k * 64 + g * 8 + 2 * t] = C[0];
-                        a.dump.coeffs[1][k * 64 + g * 8 + 2 * t + 1] = C[1];
-                        a.dump.coeffs[2][k * 64 + g * 8 + 2 * t] = C[2];
-                        a.dump.coeffs[2][k * 64 + g * 8 + 2 * t + 1] = C[3];
-                    }
-                } else {
-#pragma unroll
-                    for (int pl = 1; pl <= 2; ++pl) {
-                        const uint32_t box = pl == 1 ? boxU : boxV;
-                        uint32_t blo[2], bhi[2];
-#pragma unroll
-                        for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC, 8 * q + g, t, hvC, wvC, xpart, blo[q], bhi[q]);
-                        int32_t C[2][4];
-                        dct16<ES>(L, blo, bhi, C);
-                        double hacc = 0.0;
-#pragma unroll
-                        for (int p = 0; p < 2; ++p)
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) hacc = fma(wc[p * 4 + e], abs_to_double(C[p][e]), hacc);
-                        if (pl == 1) { huu = hacc; dcU = C[0][0]; } else { hvv = hacc; dcV = C[0][0]; }
-                        if (DUMP) {
-#pragma unroll
-                            for (int p = 0; p < 2; ++p)
-#pragma unroll
-                                for (int e = 0; e < 4; ++e)
-                                    a.dump.coeffs[pl][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
-                        }
-                    }
-                }
-                hu += huu;
-                hv += hvv;
+                const uint32_t boxY = base + (u / F::UPB_Y) * F::BOXB_Y;
+                const uint32_t boxU = base + F::ST_Y + (u / F::UPB_C) * F::BOXB_C;
+                UnitOut o;
+                if (wvY < W)
+                    process_unit<F, true, DUMP>(U, a, boxY, boxU, u % F::UPB_Y, u % F::UPB_C, hvY, hvC, wvY, wvC,
+                                                (int64_t)r * cols + c, o);
+                else
+                    process_unit<F, false, DUMP>(U, a, boxY, boxU, u % F::UPB_Y, u % F::UPB_C, hvY, hvC, wvY, wvC,
+                                                 (int64_t)r * cols + c, o);
+                hu += o.hu;
+                hv += o.hv;
                 // stash: per-unit luma row-group partials and DC sums, reduced 32 units at a time
-                const int slot = s & 31;
-                if (t == 0) hst[slot * 9 + g] = hY;
+                if (t == 0) hst[slot * 9 + g] = o.hY;
                 if (lane == 0) {
                     // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
-                    sxs[slot * 4 + 0] = (uint32_t)dcY >> 12;
-                    sxs[slot * 4 + 1] = (uint32_t)dcU >> 12;
-                    sxs[slot * 4 + 2] = (uint32_t)dcV >> 12;
-                }
-                if (DUMP) {
-#pragma unroll
-                    for (int o = 4; o < 32; o <<= 1) hY += __shfl_xor_sync(0xffffffffu, hY, o);
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        huu += __shfl_xor_sync(0xffffffffu, huu, o);
-                        hvv += __shfl_xor_sync(0xffffffffu, hvv, o);
-                    }
-                    if (lane == 0) {
-                        const uint32_t sxY = (uint32_t)dcY >> 12, sxU = (uint32_t)dcU >> 12, sxV = (uint32_t)dcV >> 12;
-                        a.dump.sumx[0][k] = sxY;
-                        a.dump.sumx[1][k] = sxU;
-                        a.dump.sumx[2][k] = sxV;
-                        a.dump.H[0][k] = hY;
-                        a.dump.H[1][k] = huu;
-                        a.dump.H[2][k] = hvv;
-                        a.dump.L[0][k] = sqrt((double)sxY * invNY);
-                        a.dump.L[1][k] = sqrt((double)sxU * invNC);
-                        a.dump.L[2][k] = sqrt((double)sxV * invNC);
-                    }
+                    sxs[slot * 4 + 0] = (uint32_t)o.dcY >> 12;
+                    sxs[slot * 4 + 1] = (uint32_t)o.dcU >> 12;
+                    sxs[slot * 4 + 2] = (uint32_t)o.dcV >> 12;
                 }
             }
-            if ((s & 31) == 31 || s == strips - 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == F::STAGES) {
+                st = 0;
+                phase ^= 1;
+            }
+            if (slot == 31 || s == strips - 1) {
                 // flush: lane l finishes unit slot l -- H_Y (fixed order over the 8 row
                 // groups), its L terms (A6), the per-block H_Y store (A5, needed for h);
                 // then a fixed xor tree over lanes into the running item sums.
-                __syncwarp();
-                const int slot = s & 31;
                 const int cl = (s - slot + lane) * F::UNITS + u;
                 double Hl = 0.0, LYl = 0.0, LUl = 0.0, LVl = 0.0;
                 if (lane <= slot && cl < cols) {
@@ -708,7 +756,7 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                     LYl = sqrt((double)sxs[lane * 4 + 0] * invNY);
                     LUl = sqrt((double)sxs[lane * 4 + 1] * invNC);
                     LVl = sqrt((double)sxs[lane * 4 + 2] * invNC);
-                    a.s.HY[(int64_t)f * rows * cols + (int64_t)r * cols + cl] = Hl;
+                    HYrow[cl] = Hl;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -723,8 +771,6 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
                 sLV += LVl;
                 __syncwarp();
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
         }
         // ---- item end: fixed-order partials of this warp's units (A7 inputs)
 #pragma unroll
