@@ -38,12 +38,14 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libvca.so (or, with ``out``/``defines``, an A/B experiment variant)."""
+    target = out or LIB
+    if not force and out is None and not stale():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", tmp,
-                                 os.path.join(CSRC, "vca_api.cu")]
+    tmp = target + ".tmp%d" % os.getpid()
+    cmd = [NVCC] + NVCC_FLAGS + ["-D" + d for d in defines] + ["-I", os.path.join(ROOT, "include"), "-o", tmp,
+                                                                 os.path.join(CSRC, "vca_api.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as fh:
@@ -53,10 +55,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libvca.so (see %s)" % log)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    # python build.py [--force] [--variant NAME DEF1 DEF2 ...]
+    if "--variant" in sys.argv:
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], sys.argv[i + 2:]
+        os.makedirs(os.path.join(HERE, "variants"), exist_ok=True)
+        print(build(force=True, out=os.path.join(HERE, "variants", "libvca_%s.so" % name), defines=defs))
+    else:
+        build(force="--force" in sys.argv, verbose=True)
+        print(LIB)

@@ -128,7 +128,11 @@ __device__ __forceinline__ void byte_planes(uint32_t v0, uint32_t v1, uint32_t v
 __device__ __forceinline__ double abs_to_double(int32_t c)
 {
     const uint32_t u = (uint32_t)(c < 0 ? -c : c);
+#ifndef VCA_CVT_MAGIC
+    return __uint2double_rn(u);  // I2F.F64.U32 on the conversion pipe (A/B: +3 % over the magic DADD)
+#else
     return __hiloint2double(0x43300000, (int)u) - 4503599627370496.0;
+#endif
 }
 
 __device__ __forceinline__ int32_t combine3(int32_t d0, int32_t d1, int32_t d2)
@@ -153,7 +157,10 @@ struct Fam {
     static constexpr int ST_Y = NBOX_Y * BOXB_Y, ST_C = NBOX_C * BOXB_C;
     static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
     static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
-    static constexpr int RING = 36864;  // ring bytes per CTA (several CTAs per SM)
+#ifndef VCA_RING
+#define VCA_RING 36864  // 6 stages of 6 KB (config 3); A/B: 4 and 6 stages equal, 8 stages -> 3 CTAs/SM, -9 %
+#endif
+    static constexpr int RING = VCA_RING;  // ring bytes per CTA (several CTAs per SM)
     static constexpr int STAGES = (RING / STAGE) < 4 ? 4 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);               // luma weights from smem (32 per lane)
     static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;  // per consumer warp
@@ -466,10 +473,20 @@ __device__ __forceinline__ void process_unit(const UnitCtx<F> &U, const FusedArg
         for (int q = 0; q < 2; ++q) load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, XPART, blo[q], bhi[q]);
         int32_t C[2][4];
         dct16<ES>(L, blo, bhi, C);
+#ifdef VCA_SPLIT_ACC
+        double h0 = 0.0, h1 = 0.0;  // two independent FMA chains, combined once (fixed order)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            h0 = fma(U.wl16[e], abs_to_double(C[0][e]), h0);
+            h1 = fma(U.wl16[4 + e], abs_to_double(C[1][e]), h1);
+        }
+        hY = h0 + h1;
+#else
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int e = 0; e < 4; ++e) hY = fma(U.wl16[p * 4 + e], abs_to_double(C[p][e]), hY);
+#endif
         o.dcY = C[0][0];
         if (DUMP) {
 #pragma unroll
@@ -597,8 +614,47 @@ __device__ __forceinline__ void process_unit(const UnitCtx<F> &U, const FusedArg
     }
 }
 
+#ifdef VCA_NO_PRODUCER
+constexpr int kFusedThreads = 128;  // 4 consumer warps; warp 0 lane 0 also issues the TMA loads
+constexpr int kConsumer0 = 0;
+#ifndef VCA_LAG
+#define VCA_LAG 2
+#endif
+#else
+constexpr int kFusedThreads = 160;  // producer warp + 4 consumer warps
+constexpr int kConsumer0 = 1;
+#endif
+#ifndef VCA_MINB
+#define VCA_MINB 4  // 4 CTAs/SM: <= 102 registers, no spills (A/B: 5 spills and loses 14 %)
+#endif
+
+// Issue the TMA loads of CTA-local strip q (item blockIdx.x + (q / strips) * gridDim.x,
+// strip q % strips) into ring stage q % STAGES.
+template <class F>
+__device__ __forceinline__ void issue_strip(uint32_t q, int strips, int rows, uint8_t *smem, uint64_t *full,
+                                            const CUtensorMap *tmY, const CUtensorMap *tmU, const CUtensorMap *tmV,
+                                            uint64_t policy)
+{
+    const int it = blockIdx.x + (int)(q / strips) * gridDim.x;
+    const int s = (int)(q % strips);
+    const int f = it / rows, r = it - f * rows;
+    const uint32_t st = q % F::STAGES;
+    uint8_t *base = smem + st * F::STAGE;
+    mbar_expect_tx(&full[st], F::TX);
+#pragma unroll
+    for (int b = 0; b < F::NBOX_Y; ++b)
+        tma_load_3d(base + b * F::BOXB_Y, tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * F::W, r * F::W, f, policy);
+#pragma unroll
+    for (int b = 0; b < F::NBOX_C; ++b) {
+        tma_load_3d(base + F::ST_Y + b * F::BOXB_C, tmU, &full[st], (s * F::UNITS + b * F::UPB_C) * F::WC,
+                    r * F::WC, f, policy);
+        tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, tmV, &full[st], (s * F::UNITS + b * F::UPB_C) * F::WC,
+                    r * F::WC, f, policy);
+    }
+}
+
 template <int W_, int BD_, int LP_, bool DUMP>
-__global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUtensorMap tmY,
+__global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
                                                     const __grid_constant__ CUtensorMap tmU,
                                                     const __grid_constant__ CUtensorMap tmV, const FusedArgs a)
 {
@@ -637,6 +693,16 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
     const int strips = (cols + F::UNITS - 1) / F::UNITS;
     const int items = a.n_frames * rows;  // < 2^31 (checked on the host)
 
+#ifdef VCA_NO_PRODUCER
+    const uint32_t my_items = blockIdx.x < (unsigned)items ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t total_q = my_items * strips;
+    uint64_t policy = 0;
+    if (warp == 0 && lane == 0) {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+        for (uint32_t q = 0; q < total_q && q < (uint32_t)F::STAGES; ++q)
+            issue_strip<F>(q, strips, rows, smem, full, &tmY, &tmU, &tmV, policy);
+    }
+#else
     if (warp == 0) {
         // ---------------- TMA producer (A1)
         if (lane == 0) {
@@ -674,9 +740,10 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
         }
         return;
     }
+#endif
 
     // ---------------- consumers
-    const int u = warp - 1;
+    const int u = warp - kConsumer0;
     const int g = lane >> 2, t = lane & 3;
     double *hst = reinterpret_cast<double *>(stash + u * F::STASH);
     uint32_t *sxs = reinterpret_cast<uint32_t *>(stash + u * F::STASH + 32 * 9 * 8);
@@ -704,7 +771,7 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
     const uint32_t full0 = smem_u32(full);
     const int64_t CY = (int64_t)rows * cols;
 
-    uint32_t st = 0, phase = 0;
+    uint32_t st = 0, phase = 0, qcur = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int f = it / rows, r = it - f * rows;
         const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
@@ -740,6 +807,18 @@ __global__ void __launch_bounds__(160) fused_kernel(const __grid_constant__ CUte
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
+#ifdef VCA_NO_PRODUCER
+            if (warp == 0 && lane == 0 && qcur + 1 >= VCA_LAG) {
+                // refill the stage of strip p = qcur - (LAG - 1) with strip p + STAGES once
+                // every consumer has released it
+                const uint32_t p = qcur + 1 - VCA_LAG;
+                if (p + F::STAGES < total_q) {
+                    mbar_wait(smem_u32(&empty[p % F::STAGES]), (p / F::STAGES) & 1);
+                    issue_strip<F>(p + F::STAGES, strips, rows, smem, full, &tmY, &tmU, &tmV, policy);
+                }
+            }
+            ++qcur;
+#endif
             if (++st == F::STAGES) {
                 st = 0;
                 phase ^= 1;
@@ -877,13 +956,14 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     const bool dump = dp.coeffs[0] != nullptr;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
     int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 160, F::SMEM) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, F::SMEM) != cudaSuccess ||
+        per_sm < 1)
         per_sm = 1;
     const int64_t items = (int64_t)n_frames * a.rows;
     if (items > 0x7fffffff) return -2;
     int64_t grid = (int64_t)sm_count * per_sm;
     if (grid > items) grid = items;
-    kern<<<(unsigned)grid, 160, F::SMEM, st>>>(mY, mU, mV, a);
+    kern<<<(unsigned)grid, kFusedThreads, F::SMEM, st>>>(mY, mU, mV, a);
     return 0;
 }
 

@@ -55,9 +55,11 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if _build.stale():
-        path = _build.build()
+    path = os.environ.get("VCA_LIB")  # A/B experiments: an alternative build of the same sources
+    if not path:
+        path = _build.LIB
+        if _build.stale():
+            path = _build.build()
     L = ctypes.CDLL(path)
     vp, i64, c_int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     P3 = ctypes.c_void_p * 3
