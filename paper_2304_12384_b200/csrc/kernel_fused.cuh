@@ -147,7 +147,8 @@ struct Fam {
     static constexpr int ES = BD == 8 ? 1 : 2;
     static constexpr int NY = LP ? W / 2 : W;
     static constexpr int NC = LP ? WC / 2 : WC;
-    static constexpr int UNITS = 4;                        // units per strip (= consumer warps)
+    static constexpr int NU = (NY == 16) ? 2 : 1;          // units per consumer warp per strip (ILP)
+    static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
     static constexpr int IB_Y = (UNITS * RB_Y) < 128 ? UNITS * RB_Y : 128;  // box inner bytes = swizzle span
     static constexpr int IB_C = (UNITS * RB_C) < 128 ? UNITS * RB_C : 128;
@@ -158,11 +159,15 @@ struct Fam {
     static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
     static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
 #ifndef VCA_RING
-#define VCA_RING 36864  // 6 stages of 6 KB (config 3); A/B: 4 and 6 stages equal, 8 stages -> 3 CTAs/SM, -9 %
+#define VCA_RING 49152  // 4 stages of 12 KB (config 3)
 #endif
     static constexpr int RING = VCA_RING;  // ring bytes per CTA (several CTAs per SM)
     static constexpr int STAGES = (RING / STAGE) < 4 ? 4 : (RING / STAGE > 16 ? 16 : RING / STAGE);
-    static constexpr bool WTAB = (NY == 32);               // luma weights from smem (32 per lane)
+    static constexpr bool WTAB = (NY == 32);
+#ifndef VCA_MINB
+#define VCA_MINB 3
+#endif
+    static constexpr int MINB = VCA_MINB;  // CTAs/SM the register budget is sized for               // luma weights from smem (32 per lane)
     static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;  // per consumer warp
     static constexpr int SMEM =
         1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + UNITS * STASH;
@@ -201,6 +206,20 @@ __device__ __forceinline__ uint2 lds64(uint32_t a)
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v)
+{
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a)
 {
@@ -455,54 +474,57 @@ struct UnitOut {
     int32_t dcY, dcU, dcV;  // C_00 (mod 2^32) in lane 0
 };
 
-// A2-A6 for one unit (Y block + U, V blocks): swizzled smem -> registers ->
-// exact integer DCT on the tensor cores -> FP64 weighted |C| partials.
-template <class F, bool XPART, bool DUMP>
-__device__ __forceinline__ void process_unit(const UnitCtx<F> &U, const FusedArgs &a, uint32_t boxY, uint32_t boxU,
-                                             int ubY, int ubC, int hvY, int hvC, int wvY, int wvC, int64_t k,
-                                             UnitOut &o)
+// A2-A6 for NU units (each: Y block + U, V blocks) of one consumer warp:
+// swizzled smem -> registers -> exact integer DCT on the tensor cores -> FP64
+// weighted |C| partials.  The NU units are independent instruction streams the
+// compiler interleaves (latency hiding within the warp).
+template <class F, bool XPART, bool DUMP, int NU>
+__device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedArgs &a, const uint32_t (&boxY)[NU],
+                                              const uint32_t (&boxU)[NU], const int (&ubY)[NU],
+                                              const int (&ubC)[NU], int hvY, int hvC, int wvY, int wvC,
+                                              const int64_t (&k)[NU], UnitOut (&o)[NU])
 {
     constexpr int NY = F::NY, NC = F::NC, ES = F::ES;
     const int g = U.g, t = U.t;
     const LaneConst &L = U.L;
-    const uint32_t boxV = boxU + F::ST_C;
-    double hY = 0.0;
+    double hY[NU];
     if (NY == 16) {
-        uint32_t blo[2], bhi[2];
+        uint32_t blo[NU][2], bhi[NU][2];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, XPART, blo[q], bhi[q]);
-        int32_t C[2][4];
-        dct16<ES>(L, blo, bhi, C);
-#ifdef VCA_SPLIT_ACC
-        double h0 = 0.0, h1 = 0.0;  // two independent FMA chains, combined once (fixed order)
+        for (int n = 0; n < NU; ++n)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            h0 = fma(U.wl16[e], abs_to_double(C[0][e]), h0);
-            h1 = fma(U.wl16[4 + e], abs_to_double(C[1][e]), h1);
-        }
-        hY = h0 + h1;
-#else
+            for (int q = 0; q < 2; ++q) load4<F, 0>(boxY[n], ubY[n], 8 * q + g, t, hvY, wvY, XPART, blo[n][q], bhi[n][q]);
+        int32_t C[NU][2][4];
 #pragma unroll
-        for (int p = 0; p < 2; ++p)
+        for (int n = 0; n < NU; ++n) dct16<ES>(L, blo[n], bhi[n], C[n]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) hY = fma(U.wl16[p * 4 + e], abs_to_double(C[p][e]), hY);
-#endif
-        o.dcY = C[0][0];
-        if (DUMP) {
+        for (int n = 0; n < NU; ++n) {
+            // |C| folds into the DFMA operand (fabs of an exact int32 -> double conversion)
+            double h0 = 0.0, h1 = 0.0;  // two FMA chains, combined once (fixed order)
 #pragma unroll
-            for (int p = 0; p < 2; ++p)
+            for (int e = 0; e < 4; ++e) {
+                h0 = fma(U.wl16[e], fabs(__int2double_rn(C[n][0][e])), h0);
+                h1 = fma(U.wl16[4 + e], fabs(__int2double_rn(C[n][1][e])), h1);
+            }
+            hY[n] = h0 + h1;
+            o[n].dcY = C[n][0][0];
+            if (DUMP) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    a.dump.coeffs[0][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        a.dump.coeffs[0][k[n] * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[n][p][e];
+            }
         }
     } else {
+        static_assert(NY != 32 || NU == 1, "n = 32 luma runs one unit per warp");
         // n = 32: pass 1 over 4 n-tiles (y = 8q + g), 2 m-tiles (j = 16mt + g (+8))
         int32_t D1[2][4][4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             uint32_t l0, h0, l1, h1;
-            load4<F, 0>(boxY, ubY, 8 * q + g, t, hvY, wvY, XPART, l0, h0);
-            load4<F, 0>(boxY, ubY, 8 * q + g, 4 + t, hvY, wvY, XPART, l1, h1);
+            load4<F, 0>(boxY[0], ubY[0], 8 * q + g, t, hvY, wvY, XPART, l0, h0);
+            load4<F, 0>(boxY[0], ubY[0], 8 * q + g, 4 + t, hvY, wvY, XPART, l1, h1);
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
                 mma32_su(D1[mt][q], L.t32[mt], l0, l1);
@@ -514,6 +536,7 @@ __device__ __forceinline__ void process_unit(const UnitCtx<F> &U, const FusedArg
                 }
             }
         }
+        double hacc = 0.0;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
             const int ms = rr >> 1, hf = rr & 1;
@@ -531,135 +554,116 @@ __device__ __forceinline__ void process_unit(const UnitCtx<F> &U, const FusedArg
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int32_t cc = combine3(E0[e], E1[e], E2[e]);
-                    hY = fma(U.wtab[((mt * 4 + rr) * 4 + e) * 32], abs_to_double(cc), hY);
-                    if (mt == 0 && rr == 0 && e == 0) o.dcY = cc;
+                    hacc = fma(U.wtab[((mt * 4 + rr) * 4 + e) * 32], fabs(__int2double_rn(cc)), hacc);
+                    if (mt == 0 && rr == 0 && e == 0) o[0].dcY = cc;
                     if (DUMP)
-                        a.dump.coeffs[0][k * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
+                        a.dump.coeffs[0][k[0] * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
                 }
             }
         }
+        hY[0] = hacc;
     }
-    // reduce over the 4 lanes of a row group: lanes t == 0 hold the partial of rows g (+8, ...)
-    hY += __shfl_xor_sync(0xffffffffu, hY, 1);
-    hY += __shfl_xor_sync(0xffffffffu, hY, 2);
-    o.hY = hY;
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        // reduce over the 4 lanes of a row group: lanes t == 0 hold the partial of rows g (+8, ...)
+        hY[n] += __shfl_xor_sync(0xffffffffu, hY[n], 1);
+        hY[n] += __shfl_xor_sync(0xffffffffu, hY[n], 2);
+        o[n].hY = hY[n];
+    }
 
     // ---- chroma
     if (NC == 8) {
-        uint32_t blo, bhi;
-        load4<F, 1>(t < 2 ? boxU : boxV, ubC, g, t & 1, hvC, wvC, XPART, blo, bhi);
-        int32_t C[4];
-        dct8pair<ES>(L, blo, bhi, C);
-        o.hu = fma(U.wc[1], abs_to_double(C[1]), U.wc[0] * abs_to_double(C[0]));
-        o.hv = fma(U.wc[1], abs_to_double(C[3]), U.wc[0] * abs_to_double(C[2]));
-        o.dcU = C[0];
-        o.dcV = C[2];
-        if (DUMP) {
-            a.dump.coeffs[1][k * 64 + g * 8 + 2 * t] = C[0];
-            a.dump.coeffs[1][k * 64 + g * 8 + 2 * t + 1] = C[1];
-            a.dump.coeffs[2][k * 64 + g * 8 + 2 * t] = C[2];
-            a.dump.coeffs[2][k * 64 + g * 8 + 2 * t + 1] = C[3];
+        uint32_t blo[NU], bhi[NU];
+#pragma unroll
+        for (int n = 0; n < NU; ++n)
+            load4<F, 1>(t < 2 ? boxU[n] : boxU[n] + F::ST_C, ubC[n], g, t & 1, hvC, wvC, XPART, blo[n], bhi[n]);
+        int32_t C[NU][4];
+#pragma unroll
+        for (int n = 0; n < NU; ++n) dct8pair<ES>(L, blo[n], bhi[n], C[n]);
+#pragma unroll
+        for (int n = 0; n < NU; ++n) {
+            o[n].hu = fma(U.wc[1], fabs(__int2double_rn(C[n][1])), U.wc[0] * fabs(__int2double_rn(C[n][0])));
+            o[n].hv = fma(U.wc[1], fabs(__int2double_rn(C[n][3])), U.wc[0] * fabs(__int2double_rn(C[n][2])));
+            o[n].dcU = C[n][0];
+            o[n].dcV = C[n][2];
+            if (DUMP) {
+                a.dump.coeffs[1][k[n] * 64 + g * 8 + 2 * t] = C[n][0];
+                a.dump.coeffs[1][k[n] * 64 + g * 8 + 2 * t + 1] = C[n][1];
+                a.dump.coeffs[2][k[n] * 64 + g * 8 + 2 * t] = C[n][2];
+                a.dump.coeffs[2][k[n] * 64 + g * 8 + 2 * t + 1] = C[n][3];
+            }
         }
     } else {
+        static_assert(NC != 16 || NU == 1, "n = 16 chroma pairs with n = 32 luma");
 #pragma unroll
         for (int pl = 1; pl <= 2; ++pl) {
-            const uint32_t box = pl == 1 ? boxU : boxV;
+            const uint32_t box = pl == 1 ? boxU[0] : boxU[0] + F::ST_C;
             uint32_t blo[2], bhi[2];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC, 8 * q + g, t, hvC, wvC, XPART, blo[q], bhi[q]);
+            for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC[0], 8 * q + g, t, hvC, wvC, XPART, blo[q], bhi[q]);
             int32_t C[2][4];
             dct16<ES>(L, blo, bhi, C);
             double hacc = 0.0;
 #pragma unroll
             for (int p = 0; p < 2; ++p)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) hacc = fma(U.wc[p * 4 + e], abs_to_double(C[p][e]), hacc);
+                for (int e = 0; e < 4; ++e) hacc = fma(U.wc[p * 4 + e], fabs(__int2double_rn(C[p][e])), hacc);
             if (pl == 1) {
-                o.hu = hacc;
-                o.dcU = C[0][0];
+                o[0].hu = hacc;
+                o[0].dcU = C[0][0];
             } else {
-                o.hv = hacc;
-                o.dcV = C[0][0];
+                o[0].hv = hacc;
+                o[0].dcV = C[0][0];
             }
             if (DUMP) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p)
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        a.dump.coeffs[pl][k * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+                        a.dump.coeffs[pl][k[0] * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
             }
         }
     }
     if (DUMP) {
-        double hy = hY, hu = o.hu, hv = o.hv;
 #pragma unroll
-        for (int s = 4; s < 32; s <<= 1) hy += __shfl_xor_sync(0xffffffffu, hy, s);
+        for (int n = 0; n < NU; ++n) {
+            double hy = hY[n], hu = o[n].hu, hv = o[n].hv;
 #pragma unroll
-        for (int s = 16; s > 0; s >>= 1) {
-            hu += __shfl_xor_sync(0xffffffffu, hu, s);
-            hv += __shfl_xor_sync(0xffffffffu, hv, s);
-        }
-        if (g == 0 && t == 0) {
-            const uint32_t sxY = (uint32_t)o.dcY >> 12, sxU = (uint32_t)o.dcU >> 12, sxV = (uint32_t)o.dcV >> 12;
-            a.dump.sumx[0][k] = sxY;
-            a.dump.sumx[1][k] = sxU;
-            a.dump.sumx[2][k] = sxV;
-            a.dump.H[0][k] = hy;
-            a.dump.H[1][k] = hu;
-            a.dump.H[2][k] = hv;
-            a.dump.L[0][k] = sqrt((double)sxY * (1.0 / NY));
-            a.dump.L[1][k] = sqrt((double)sxU * (1.0 / NC));
-            a.dump.L[2][k] = sqrt((double)sxV * (1.0 / NC));
+            for (int s = 4; s < 32; s <<= 1) hy += __shfl_xor_sync(0xffffffffu, hy, s);
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                hu += __shfl_xor_sync(0xffffffffu, hu, s);
+                hv += __shfl_xor_sync(0xffffffffu, hv, s);
+            }
+            if (g == 0 && t == 0) {
+                const uint32_t sxY = (uint32_t)o[n].dcY >> 12, sxU = (uint32_t)o[n].dcU >> 12,
+                               sxV = (uint32_t)o[n].dcV >> 12;
+                const int64_t kk = k[n];
+                a.dump.sumx[0][kk] = sxY;
+                a.dump.sumx[1][kk] = sxU;
+                a.dump.sumx[2][kk] = sxV;
+                a.dump.H[0][kk] = hy;
+                a.dump.H[1][kk] = hu;
+                a.dump.H[2][kk] = hv;
+                a.dump.L[0][kk] = sqrt((double)sxY * (1.0 / NY));
+                a.dump.L[1][kk] = sqrt((double)sxU * (1.0 / NC));
+                a.dump.L[2][kk] = sqrt((double)sxV * (1.0 / NC));
+            }
         }
     }
 }
 
-#ifdef VCA_NO_PRODUCER
-constexpr int kFusedThreads = 128;  // 4 consumer warps; warp 0 lane 0 also issues the TMA loads
-constexpr int kConsumer0 = 0;
-#ifndef VCA_LAG
-#define VCA_LAG 2
-#endif
-#else
 constexpr int kFusedThreads = 160;  // producer warp + 4 consumer warps
 constexpr int kConsumer0 = 1;
-#endif
-#ifndef VCA_MINB
-#define VCA_MINB 4  // 4 CTAs/SM: <= 102 registers, no spills (A/B: 5 spills and loses 14 %)
-#endif
-
-// Issue the TMA loads of CTA-local strip q (item blockIdx.x + (q / strips) * gridDim.x,
-// strip q % strips) into ring stage q % STAGES.
-template <class F>
-__device__ __forceinline__ void issue_strip(uint32_t q, int strips, int rows, uint8_t *smem, uint64_t *full,
-                                            const CUtensorMap *tmY, const CUtensorMap *tmU, const CUtensorMap *tmV,
-                                            uint64_t policy)
-{
-    const int it = blockIdx.x + (int)(q / strips) * gridDim.x;
-    const int s = (int)(q % strips);
-    const int f = it / rows, r = it - f * rows;
-    const uint32_t st = q % F::STAGES;
-    uint8_t *base = smem + st * F::STAGE;
-    mbar_expect_tx(&full[st], F::TX);
-#pragma unroll
-    for (int b = 0; b < F::NBOX_Y; ++b)
-        tma_load_3d(base + b * F::BOXB_Y, tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * F::W, r * F::W, f, policy);
-#pragma unroll
-    for (int b = 0; b < F::NBOX_C; ++b) {
-        tma_load_3d(base + F::ST_Y + b * F::BOXB_C, tmU, &full[st], (s * F::UNITS + b * F::UPB_C) * F::WC,
-                    r * F::WC, f, policy);
-        tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, tmV, &full[st], (s * F::UNITS + b * F::UPB_C) * F::WC,
-                    r * F::WC, f, policy);
-    }
-}
+constexpr int kConsumers = 4;
 
 template <int W_, int BD_, int LP_, bool DUMP>
-__global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
+__global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
                                                     const __grid_constant__ CUtensorMap tmU,
                                                     const __grid_constant__ CUtensorMap tmV, const FusedArgs a)
 {
     using F = Fam<W_, BD_, LP_>;
-    constexpr int NY = F::NY, NC = F::NC, ES = F::ES, W = F::W, WC = F::WC;
+    constexpr int NY = F::NY, NC = F::NC, W = F::W, WC = F::WC, NU = F::NU;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + F::STAGES * F::STAGE);
@@ -672,7 +676,7 @@ __global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __
     if (threadIdx.x == 0) {
         for (int i = 0; i < F::STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], F::UNITS);
+            mbar_init(&empty[i], kConsumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -693,16 +697,6 @@ __global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __
     const int strips = (cols + F::UNITS - 1) / F::UNITS;
     const int items = a.n_frames * rows;  // < 2^31 (checked on the host)
 
-#ifdef VCA_NO_PRODUCER
-    const uint32_t my_items = blockIdx.x < (unsigned)items ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const uint32_t total_q = my_items * strips;
-    uint64_t policy = 0;
-    if (warp == 0 && lane == 0) {
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-        for (uint32_t q = 0; q < total_q && q < (uint32_t)F::STAGES; ++q)
-            issue_strip<F>(q, strips, rows, smem, full, &tmY, &tmU, &tmV, policy);
-    }
-#else
     if (warp == 0) {
         // ---------------- TMA producer (A1)
         if (lane == 0) {
@@ -740,13 +734,12 @@ __global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __
         }
         return;
     }
-#endif
 
     // ---------------- consumers
     const int u = warp - kConsumer0;
     const int g = lane >> 2, t = lane & 3;
-    double *hst = reinterpret_cast<double *>(stash + u * F::STASH);
-    uint32_t *sxs = reinterpret_cast<uint32_t *>(stash + u * F::STASH + 32 * 9 * 8);
+    const uint32_t hst = smem_u32(stash) + u * F::STASH;  // [32][9] doubles
+    const uint32_t sxs = hst + 32 * 9 * 8;                 // [32][4] uint32
     UnitCtx<F> U;
     build_lane_const(U.L, a.T_all, g, t, NY);
     // per-lane scaled weights (A5): luma n = 16 positions (i = g + 8(e>>1), j = 8p + 2t + (e&1)),
@@ -771,7 +764,7 @@ __global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __
     const uint32_t full0 = smem_u32(full);
     const int64_t CY = (int64_t)rows * cols;
 
-    uint32_t st = 0, phase = 0, qcur = 0;
+    uint32_t st = 0, phase = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int f = it / rows, r = it - f * rows;
         const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
@@ -780,61 +773,86 @@ __global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __
         double *HYrow = a.s.HY + (int64_t)f * CY + (int64_t)r * cols;
         for (int s = 0; s < strips; ++s) {
             mbar_wait(full0 + 8 * st, phase);
-            const int c = s * F::UNITS + u;
-            const int slot = s & 31;
-            if (c < cols) {
-                const uint32_t base = smem0 + st * F::STAGE;
-                const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
-                const uint32_t boxY = base + (u / F::UPB_Y) * F::BOXB_Y;
-                const uint32_t boxU = base + F::ST_Y + (u / F::UPB_C) * F::BOXB_C;
-                UnitOut o;
-                if (wvY < W)
-                    process_unit<F, true, DUMP>(U, a, boxY, boxU, u % F::UPB_Y, u % F::UPB_C, hvY, hvC, wvY, wvC,
-                                                (int64_t)r * cols + c, o);
-                else
-                    process_unit<F, false, DUMP>(U, a, boxY, boxU, u % F::UPB_Y, u % F::UPB_C, hvY, hvC, wvY, wvC,
-                                                 (int64_t)r * cols + c, o);
-                hu += o.hu;
-                hv += o.hv;
+            // this warp's units of strip s: c_n = s*UNITS + u + 4n, n < NU, in ascending order;
+            // unit m = s*NU + n of the item goes to stash slot m & 31
+            const uint32_t base = smem0 + st * F::STAGE;
+            const int c0 = s * F::UNITS + u;
+#ifndef VCA_NULL_COMPUTE
+            const bool full_group = c0 + 4 * (NU - 1) < cols && a.width[0] - (c0 + 4 * (NU - 1)) * W >= W;
+            UnitOut o[NU];
+            bool valid[NU];
+            if (full_group) {
+                uint32_t bY[NU], bU[NU];
+                int uY[NU], uC[NU];
+                int64_t kk[NU];
+#pragma unroll
+                for (int n = 0; n < NU; ++n) {
+                    const int v = u + 4 * n;  // unit index within the strip
+                    bY[n] = base + (v / F::UPB_Y) * F::BOXB_Y;
+                    bU[n] = base + F::ST_Y + (v / F::UPB_C) * F::BOXB_C;
+                    uY[n] = v % F::UPB_Y;
+                    uC[n] = v % F::UPB_C;
+                    kk[n] = (int64_t)r * cols + c0 + 4 * n;
+                    valid[n] = true;
+                }
+                process_units<F, false, DUMP, NU>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o);
+            } else {
+                // ragged strip end or a partial last block column: one unit at a time
+#pragma unroll
+                for (int n = 0; n < NU; ++n) {
+                    const int c = c0 + 4 * n;
+                    valid[n] = c < cols;
+                    if (!valid[n]) continue;
+                    const int v = u + 4 * n;
+                    const uint32_t bY[1] = {base + (v / F::UPB_Y) * F::BOXB_Y};
+                    const uint32_t bU[1] = {base + F::ST_Y + (v / F::UPB_C) * F::BOXB_C};
+                    const int uY[1] = {v % F::UPB_Y}, uC[1] = {v % F::UPB_C};
+                    const int64_t kk[1] = {(int64_t)r * cols + c};
+                    const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
+                    UnitOut o1[1];
+                    if (wvY < W)
+                        process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1);
+                    else
+                        process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1);
+                    o[n] = o1[0];
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < NU; ++n) {
+                if (!valid[n]) continue;
+                const int slot = (s * NU + n) & 31;
+                hu += o[n].hu;
+                hv += o[n].hv;
                 // stash: per-unit luma row-group partials and DC sums, reduced 32 units at a time
-                if (t == 0) hst[slot * 9 + g] = o.hY;
+                if (t == 0) sts_f64(hst + (slot * 9 + g) * 8, o[n].hY);
                 if (lane == 0) {
                     // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
-                    sxs[slot * 4 + 0] = (uint32_t)o.dcY >> 12;
-                    sxs[slot * 4 + 1] = (uint32_t)o.dcU >> 12;
-                    sxs[slot * 4 + 2] = (uint32_t)o.dcV >> 12;
+                    sts_u32(sxs + slot * 16 + 0, (uint32_t)o[n].dcY >> 12);
+                    sts_u32(sxs + slot * 16 + 4, (uint32_t)o[n].dcU >> 12);
+                    sts_u32(sxs + slot * 16 + 8, (uint32_t)o[n].dcV >> 12);
                 }
             }
+#endif
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
-#ifdef VCA_NO_PRODUCER
-            if (warp == 0 && lane == 0 && qcur + 1 >= VCA_LAG) {
-                // refill the stage of strip p = qcur - (LAG - 1) with strip p + STAGES once
-                // every consumer has released it
-                const uint32_t p = qcur + 1 - VCA_LAG;
-                if (p + F::STAGES < total_q) {
-                    mbar_wait(smem_u32(&empty[p % F::STAGES]), (p / F::STAGES) & 1);
-                    issue_strip<F>(p + F::STAGES, strips, rows, smem, full, &tmY, &tmU, &tmV, policy);
-                }
-            }
-            ++qcur;
-#endif
             if (++st == F::STAGES) {
                 st = 0;
                 phase ^= 1;
             }
-            if (slot == 31 || s == strips - 1) {
-                // flush: lane l finishes unit slot l -- H_Y (fixed order over the 8 row
-                // groups), its L terms (A6), the per-block H_Y store (A5, needed for h);
-                // then a fixed xor tree over lanes into the running item sums.
-                const int cl = (s - slot + lane) * F::UNITS + u;
+            const int mlast = s * NU + NU - 1;  // last unit index of this strip
+            if ((mlast & 31) == 31 || s == strips - 1) {
+                // flush: lane l finishes unit m = mlast - (mlast & 31) + l -- H_Y (fixed order
+                // over the 8 row groups), its L terms (A6), the per-block H_Y store (A5, needed
+                // for h); then a fixed xor tree over lanes into the running item sums.
+                const int m = mlast - (mlast & 31) + lane;
+                const int cl = (m / NU) * F::UNITS + u + 4 * (m % NU);
                 double Hl = 0.0, LYl = 0.0, LUl = 0.0, LVl = 0.0;
-                if (lane <= slot && cl < cols) {
+                if (lane <= (mlast & 31) && cl < cols) {
 #pragma unroll
-                    for (int gg = 0; gg < 8; ++gg) Hl += hst[lane * 9 + gg];
-                    LYl = sqrt((double)sxs[lane * 4 + 0] * invNY);
-                    LUl = sqrt((double)sxs[lane * 4 + 1] * invNC);
-                    LVl = sqrt((double)sxs[lane * 4 + 2] * invNC);
+                    for (int gg = 0; gg < 8; ++gg) Hl += lds_f64(hst + (lane * 9 + gg) * 8);
+                    LYl = sqrt((double)lds32(sxs + lane * 16 + 0) * invNY);
+                    LUl = sqrt((double)lds32(sxs + lane * 16 + 4) * invNC);
+                    LVl = sqrt((double)lds32(sxs + lane * 16 + 8) * invNC);
                     HYrow[cl] = Hl;
                 }
 #pragma unroll
@@ -858,7 +876,7 @@ __global__ void __launch_bounds__(kFusedThreads, VCA_MINB) fused_kernel(const __
             hv += __shfl_xor_sync(0xffffffffu, hv, o);
         }
         if (lane == 0) {
-            const int64_t q = (int64_t)r * F::UNITS + u;
+            const int64_t q = (int64_t)r * kConsumers + u;
             double *P0 = a.s.partial + (((int64_t)f * 3 + 0) * a.s.P + q) * 2;
             double *P1 = a.s.partial + (((int64_t)f * 3 + 1) * a.s.P + q) * 2;
             double *P2 = a.s.partial + (((int64_t)f * 3 + 2) * a.s.P + q) * 2;

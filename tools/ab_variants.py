@@ -17,16 +17,34 @@ from paper_2304_12384_b200 import synth, vca  # noqa: E402
 
 
 def main():
+    """Parent: run every variant in its own process under a timeout (a hung kernel
+    must not hang the whole call).  Child (--one PATH): time one variant."""
+    if "--one" not in sys.argv:
+        import subprocess
+        libs = sys.argv[1:] or sorted(glob.glob(os.path.join(ROOT, "paper_2304_12384_b200", "variants", "*.so")))
+        for rnd in range(2):
+            for path in libs:
+                try:
+                    r = subprocess.run([sys.executable, __file__, "--one", path, str(rnd)], capture_output=True,
+                                       text=True, timeout=int(os.environ.get("AB_TIMEOUT", "120")))
+                    sys.stdout.write(r.stdout + (r.stderr[-2000:] if r.returncode else ""))
+                except subprocess.TimeoutExpired:
+                    print("round %d %-28s TIMEOUT" % (rnd, os.path.basename(path)))
+                sys.stdout.flush()
+        return
+    one(sys.argv[sys.argv.index("--one") + 1], int(sys.argv[-1]))
+
+
+def one(path, rnd):
     cfg = int(os.environ.get("AB_CONFIG", "3"))
     frames = int(os.environ.get("AB_FRAMES", "600"))
     steps = int(os.environ.get("AB_STEPS", "20"))
-    libs = sys.argv[1:] or sorted(glob.glob(os.path.join(ROOT, "paper_2304_12384_b200", "variants", "*.so")))
     c = synth.CONFIGS[cfg]
     Y, U, V = synth.config_frames(cfg, device="cuda", n_frames=frames)
     fb = (c.width * c.height + 2 * (c.width // 2) * (c.height // 2)) * (1 if c.bit_depth == 8 else 2)
     ref = None
-    for rnd in range(2):
-        for path in libs:
+    for _ in (0,):
+        for path in (path,):
             vca._lib = None
             os.environ["VCA_LIB"] = path
             a = vca.Analyzer(c.width, c.height, c.bit_depth, c.block_size, c.lowpass)
@@ -47,10 +65,12 @@ def main():
             blk, fin, n = a.profile_read()
             ms = e0.elapsed_time(e1) / steps
             rec = vca.records_to_numpy(out)
-            same = ""
-            if ref is None:
-                ref = rec
+            refp = os.path.join(ROOT, "gpurun_out", "ab_ref_%d_%d.npy" % (cfg, frames))
+            if not os.path.exists(refp):
+                np.save(refp, rec)
+                same = "(reference)"
             else:
+                ref = np.load(refp)
                 same = "identical" if np.array_equal(rec, ref) else (
                     "maxrel %.3g" % max(float(np.max(np.abs(rec[f] - ref[f]) / np.maximum(np.abs(ref[f]), 1e-300)))
                                         for f in vca.FEATURES))
