@@ -147,7 +147,10 @@ struct Fam {
     static constexpr int ES = BD == 8 ? 1 : 2;
     static constexpr int NY = LP ? W / 2 : W;
     static constexpr int NC = LP ? WC / 2 : WC;
-    static constexpr int NU = (NY == 16) ? 2 : 1;          // units per consumer warp per strip (ILP)
+#ifndef VCA_NU
+#define VCA_NU 2
+#endif
+    static constexpr int NU = (NY == 16) ? VCA_NU : 1;     // units per consumer warp per strip (ILP)
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
     static constexpr int IB_Y = (UNITS * RB_Y) < 128 ? UNITS * RB_Y : 128;  // box inner bytes = swizzle span
@@ -159,10 +162,10 @@ struct Fam {
     static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
     static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
 #ifndef VCA_RING
-#define VCA_RING 49152  // 4 stages of 12 KB (config 3)
+#define VCA_RING 36864  // 3 stages of 12 KB (config 3); A/B: 3, 4 stages equal, 5 -> 2 CTAs/SM, -16 %
 #endif
     static constexpr int RING = VCA_RING;  // ring bytes per CTA (several CTAs per SM)
-    static constexpr int STAGES = (RING / STAGE) < 4 ? 4 : (RING / STAGE > 16 ? 16 : RING / STAGE);
+    static constexpr int STAGES = (RING / STAGE) < 2 ? 2 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);
 #ifndef VCA_MINB
 #define VCA_MINB 3
@@ -170,7 +173,7 @@ struct Fam {
     static constexpr int MINB = VCA_MINB;  // CTAs/SM the register budget is sized for               // luma weights from smem (32 per lane)
     static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;  // per consumer warp
     static constexpr int SMEM =
-        1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + UNITS * STASH;
+        1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + 4 * STASH;
     static_assert(NC == NY / 2, "chroma DCT is half the luma DCT");
     static_assert(IB_Y == 32 || IB_Y == 64 || IB_Y == 128, "swizzle span");
     static_assert(IB_C == 32 || IB_C == 64 || IB_C == 128, "swizzle span");
@@ -653,8 +656,8 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     }
 }
 
-constexpr int kFusedThreads = 160;  // producer warp + 4 consumer warps
-constexpr int kConsumer0 = 1;
+constexpr int kFusedThreads = 160;  // producer warp + 4 consumer warps (A/B: a producer-less
+constexpr int kConsumer0 = 1;       // ring refilled by the last releasing warp lost 16 %)
 constexpr int kConsumers = 4;
 
 template <int W_, int BD_, int LP_, bool DUMP>
