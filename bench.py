@@ -203,10 +203,11 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2304_12384_b200 import Analyzer, records_to_numpy, synth
+    from paper_2304_12384_b200 import Analyzer, records_to_numpy, shard, synth
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -217,32 +218,35 @@ def main():
     c = synth.CONFIGS[cfg_id]
     W, H, bd = c.width, c.height, c.bit_depth
     F = args.frames
-    # --- inputs (outside timing): rank r = segment r of config 5 for N > 1
+    # --- inputs (outside timing).  N > 1: config 5's first N segments (N x 600 frames),
+    # contiguous POC ranges per rank with a one-frame halo (paper_2304_12384_b200.shard)
     if world == 1:
         Y, U, V = synth.config_frames(cfg_id, device=dev, n_frames=F)
         n_halo = 0
         workload = "config%d_%s_%df" % (cfg_id, c.name, F)
         first_poc = 0
+        counts = None
     else:
-        n_halo = 1 if rank > 0 else 0
-        first = rank * SEG - n_halo
-        Y, U, V = synth.config_frames(5, device=dev, n_frames=F + n_halo, first_t=first)
+        sh = shard.plan(world * F, world, rank)
+        n_halo = sh.n_halo
+        Y, U, V = synth.config_frames(5, device=dev, n_frames=sh.n_frames, first_t=sh.first_frame)
         workload = "config5_%s_%dx%df" % (synth.CONFIGS[5].name, world, F)
-        first_poc = rank * SEG
+        first_poc = sh.first_poc
+        counts = [shard.plan(world * F, world, r).count for r in range(world)]
     torch.cuda.synchronize()
 
     an = Analyzer(W, H, bd, c.block_size, c.lowpass)
     nfr = Y.shape[0]
     out = torch.empty((nfr - n_halo, 8), dtype=torch.float64, device=dev)
     scratch = torch.empty(an.scratch_bytes(nfr) // 8 + 1, dtype=torch.float64, device=dev)
-    gathered = torch.empty((world * (nfr - n_halo), 8), dtype=torch.float64, device=dev) if world > 1 else None
     stream = torch.cuda.current_stream(dev)
+    gathered = [None]
 
     def step():
         an.reset(first_poc)
         an.analyze(Y, U, V, n_halo=n_halo, out=out, scratch=scratch, stream=stream)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out)
+            gathered[0] = shard.gather_records(out, world, counts=counts)
 
     for _ in range(args.warmup):
         step()
@@ -341,7 +345,8 @@ def main():
                                 "sample": "%d frames of the same workload, %.1f s, OpenMP over frames" % (n, dt)}
     if rank == 0:
         # parity spot check of the timed output (first and last record) is done in tests; here sanity only
-        rec = records_to_numpy(gathered if world > 1 else out)
+        rec = records_to_numpy(gathered[0] if world > 1 else out)
+        assert np.array_equal(rec["poc"], np.arange(len(rec))), "records out of POC order"
         line["sanity"] = {"records": int(len(rec)), "first_poc": int(rec["poc"][0]), "last_poc": int(rec["poc"][-1]),
                           "mean_E_Y": float(rec["E_Y"].mean())}
         print(json.dumps(line), flush=True)
