@@ -111,6 +111,17 @@ __device__ __forceinline__ void mma32_ss(int32_t (&d)[4], const uint32_t (&a)[4]
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0), "r"(0), "r"(0), "r"(0));
 }
 
+// D = A(u8) . B(u8) + C, m16n8k32 (the 2x2 low-pass sums, C = rounding offset)
+__device__ __forceinline__ void mma32_uu_acc(int32_t (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                             const int32_t (&c)[4])
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]));
+}
+
 // byte planes b = 0, 1, 2 of four int32 values (v0..v3 -> bytes 0..3 of each plane)
 __device__ __forceinline__ void byte_planes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t &p0,
                                             uint32_t &p1, uint32_t &p2)
@@ -173,7 +184,7 @@ struct Fam {
     static constexpr int MINB = VCA_MINB;  // CTAs/SM the register budget is sized for               // luma weights from smem (32 per lane)
     static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;  // per consumer warp
     static constexpr int SMEM =
-        1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + 4 * STASH;
+        1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + 4 * STASH + 10 * 32 * 8;
     static_assert(NC == NY / 2, "chroma DCT is half the luma DCT");
     static_assert(IB_Y == 32 || IB_Y == 64 || IB_Y == 128, "swizzle span");
     static_assert(IB_C == 32 || IB_C == 64 || IB_C == 128, "swizzle span");
@@ -250,6 +261,15 @@ __device__ __forceinline__ uint32_t ds8(uint2 a, uint2 b)
     const uint32_t sl = (a.x & M) + __byte_perm(a.x, 0u, 0x4341) + (b.x & M) + __byte_perm(b.x, 0u, 0x4341) + 0x00020002u;
     const uint32_t sh = (a.y & M) + __byte_perm(a.y, 0u, 0x4341) + (b.y & M) + __byte_perm(b.y, 0u, 0x4341) + 0x00020002u;
     return __byte_perm(sl >> 2, sh >> 2, 0x6420);
+}
+
+// four (2x2 sum + 2) values < 1024 -> packed bytes (s >> 2): low halves paired by PRMT,
+// one shift per pair, byte 0 / byte 2 of each picked by the final PRMT
+__device__ __forceinline__ uint32_t pack_ds(int32_t s0, int32_t s1, int32_t s2, int32_t s3)
+{
+    const uint32_t t01 = __byte_perm((uint32_t)s0, (uint32_t)s1, 0x5410);
+    const uint32_t t23 = __byte_perm((uint32_t)s2, (uint32_t)s3, 0x5410);
+    return __byte_perm(t01 >> 2, t23 >> 2, 0x6420);
 }
 
 __device__ __forceinline__ uint32_t pair_sum16(uint32_t v)
@@ -331,6 +351,9 @@ struct LaneConst {
     uint32_t t8a0, t8a1, p8a0, p8a1;
     // n = 32 (m16n8k32), per m-tile
     uint32_t t32[2][4], p32[2][4];
+    // 2x2 low-pass as an MMA: B = 0/1 pair-sum matrix, k = 4t+i (+16) -> source column,
+    // n = g -> output column; luma rl = [2t + (i>>1) == g], chroma rc = same over 16 columns
+    uint32_t rl, rc;
 };
 
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d)
@@ -372,6 +395,13 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
         L.p8a0 = pack4(u[0], u[1], u[2], u[3]);
         L.p8a1 = pack4(v[0], v[1], v[2], v[3]);
     }
+    {
+        uint32_t r = 0;
+        for (int i = 0; i < 4; ++i)
+            if (2 * t + (i >> 1) == g) r |= 1u << (8 * i);
+        L.rl = r;
+        L.rc = r;
+    }
     if (NY == 32) {
         const int8_t *T32 = T_all + table_offset(32);
         auto T32a = [&](int i, int x) { return (int)__ldg(T32 + i * 32 + x); };
@@ -396,14 +426,19 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
 // ------------------------------------------------------------------ DCT building blocks
 // n = 16: B fragments (lo/hi) for pass-1 n-tiles q = 0, 1 (y = 8q + g, x = 4t..4t+3)
 // -> C[p][e]: i = g + 8(e>>1), j = 8p + 2t + (e&1).
-template <int ES>
+// PERM1: the B fragments hold x in the pi16 slot order (tensor-core low-pass output),
+// so pass 1 uses the column-permuted basis T16[:, pi16] -- the same constant as pass 2.
+template <int ES, bool PERM1 = false>
 __device__ __forceinline__ void dct16(const LaneConst &L, const uint32_t (&blo)[2], const uint32_t (&bhi)[2],
                                       int32_t (&C)[2][4])
 {
     int32_t D1[2][4];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        mma16_su(D1[q], L.t16a0, L.t16a1, blo[q]);
+        if (PERM1)
+            mma16_su(D1[q], L.p16a0, L.p16a1, blo[q]);
+        else
+            mma16_su(D1[q], L.t16a0, L.t16a1, blo[q]);
         if (ES == 2) {
             int32_t Dh[4];
             mma16_su(Dh, L.t16a0, L.t16a1, bhi[q]);
@@ -426,11 +461,14 @@ __device__ __forceinline__ void dct16(const LaneConst &L, const uint32_t (&blo)[
 
 // paired n = 8 (U rows 0-7 | V rows 8-15): one B fragment (thread t < 2: U x = 4t..,
 // t >= 2: V x = 4(t-2)..; y = g) -> C[e]: e=0,1: U (i = g, j = 2t+e); e=2,3: V (i = g, j = 2t+e-2)
-template <int ES>
+template <int ES, bool PERM1 = false>
 __device__ __forceinline__ void dct8pair(const LaneConst &L, uint32_t blo, uint32_t bhi, int32_t (&C)[4])
 {
     int32_t D1[4];
-    mma16_su(D1, L.t8a0, L.t8a1, blo);
+    if (PERM1)
+        mma16_su(D1, L.p8a0, L.p8a1, blo);  // slot 4t+i = (U|V by i>>1, x = 2t + (i&1))
+    else
+        mma16_su(D1, L.t8a0, L.t8a1, blo);
     if (ES == 2) {
         int32_t Dh[4];
         mma16_su(Dh, L.t8a0, L.t8a1, bhi);
@@ -468,6 +506,7 @@ struct UnitCtx {
     double wl16[8];     // luma n = 16 weights at this lane's 8 positions
     double wc[NWC];     // chroma weights at this lane's positions
     const double *wtab; // luma n = 32 weights in smem, [slot][lane] + lane
+    uint32_t wsm;       // smem address of this lane's n = 16 / 8 weights ([e][lane])
     int g, t;
 };
 
@@ -481,6 +520,12 @@ struct UnitOut {
 // swizzled smem -> registers -> exact integer DCT on the tensor cores -> FP64
 // weighted |C| partials.  The NU units are independent instruction streams the
 // compiler interleaves (latency hiding within the warp).
+#ifdef VCA_MMA_DS
+constexpr bool kMmaDownsample = true;   // A/B: 2x2 low-pass sums as a 0/1 IMMA (exact, but its
+#else                                   // latency sits on the critical path: -4 % vs the ALUs)
+constexpr bool kMmaDownsample = false;
+#endif
+
 template <class F, bool XPART, bool DUMP, int NU>
 __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedArgs &a, const uint32_t (&boxY)[NU],
                                               const uint32_t (&boxU)[NU], const int (&ubY)[NU],
@@ -490,24 +535,77 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     constexpr int NY = F::NY, NC = F::NC, ES = F::ES;
     const int g = U.g, t = U.t;
     const LaneConst &L = U.L;
+#ifndef VCA_WREG
+    // weights from smem ([e][lane] doubles, conflict-free), loaded once per call
+    double wl[8], wcc[2];
+    if (NY == 16 && NC == 8) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) wl[e] = lds_f64(U.wsm + e * 256);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) wcc[e] = lds_f64(U.wsm + (8 + e) * 256);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) wl[e] = U.wl16[e];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) wcc[e] = U.wc[e];
+    }
+#define VCA_WL(e) wl[e]
+#define VCA_WC(e) wcc[e]
+#else
+#define VCA_WL(e) U.wl16[e]
+#define VCA_WC(e) U.wc[e]
+#endif
     double hY[NU];
+    // 8-bit low-pass on whole columns: the 2x2 sums run on the tensor cores (A3 as an
+    // exact 0/1 contraction, rounding offset as the accumulator init)
+    constexpr bool MMA_DS = F::LP && ES == 1 && !XPART && kMmaDownsample;
     if (NY == 16) {
         uint32_t blo[NU][2], bhi[NU][2];
+        if (MMA_DS) {
+            // S^T[y][x] = sum_{parity, col} px(2y + parity, col) [col/2 == x]: M = y (16),
+            // N = x (2 n-tiles), K = 2 x 32 (row parity x source column)
+            const int32_t two[4] = {2, 2, 2, 2};
 #pragma unroll
-        for (int n = 0; n < NU; ++n)
+            for (int n = 0; n < NU; ++n) {
+                int32_t S[2][4];
+                uint32_t A[2][4];
+                const int ub0 = ubY[n] * F::RB_Y;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) load4<F, 0>(boxY[n], ubY[n], 8 * q + g, t, hvY, wvY, XPART, blo[n][q], bhi[n][q]);
+                for (int par = 0; par < 2; ++par) {
+                    const int r0 = min(2 * g + par, hvY - 1), r1 = min(2 * (g + 8) + par, hvY - 1);
+                    A[par][0] = lds32(boxY[n] + swz<F::IB_Y>(r0 * F::IB_Y + ub0 + 4 * t));
+                    A[par][1] = lds32(boxY[n] + swz<F::IB_Y>(r1 * F::IB_Y + ub0 + 4 * t));
+                    A[par][2] = lds32(boxY[n] + swz<F::IB_Y>(r0 * F::IB_Y + ub0 + 16 + 4 * t));
+                    A[par][3] = lds32(boxY[n] + swz<F::IB_Y>(r1 * F::IB_Y + ub0 + 16 + 4 * t));
+                }
+                // n-tile 0 (x = g): source columns 0..15 only; n-tile 1 (x = 8 + g): 16..31
+                mma32_uu_acc(S[0], A[0], L.rl, 0u, two);
+                mma32_uu_acc(S[0], A[1], L.rl, 0u, S[0]);
+                mma32_uu_acc(S[1], A[0], 0u, L.rl, two);
+                mma32_uu_acc(S[1], A[1], 0u, L.rl, S[1]);
+                // pass-1 B fragments in pi16 slot order: y = g from c0, c1; y = g + 8 from c2, c3
+                blo[n][0] = pack_ds(S[0][0], S[0][1], S[1][0], S[1][1]);
+                blo[n][1] = pack_ds(S[0][2], S[0][3], S[1][2], S[1][3]);
+                bhi[n][0] = bhi[n][1] = 0;
+            }
+        } else {
+#pragma unroll
+            for (int n = 0; n < NU; ++n)
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    load4<F, 0>(boxY[n], ubY[n], 8 * q + g, t, hvY, wvY, XPART, blo[n][q], bhi[n][q]);
+        }
         int32_t C[NU][2][4];
 #pragma unroll
-        for (int n = 0; n < NU; ++n) dct16<ES>(L, blo[n], bhi[n], C[n]);
+        for (int n = 0; n < NU; ++n) dct16<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             // |C| folds into the DFMA operand (fabs of an exact int32 -> double conversion)
             double h0 = 0.0, h1 = 0.0;  // two FMA chains, combined once (fixed order)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                h0 = fma(U.wl16[e], fabs(__int2double_rn(C[n][0][e])), h0);
-                h1 = fma(U.wl16[4 + e], fabs(__int2double_rn(C[n][1][e])), h1);
+                h0 = fma(VCA_WL(e), fabs(__int2double_rn(C[n][0][e])), h0);
+                h1 = fma(VCA_WL(4 + e), fabs(__int2double_rn(C[n][1][e])), h1);
             }
             hY[n] = h0 + h1;
             o[n].dcY = C[n][0][0];
@@ -577,16 +675,36 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     // ---- chroma
     if (NC == 8) {
         uint32_t blo[NU], bhi[NU];
+        if (MMA_DS) {
+            // M = 16 (U rows y = m | V rows y = m - 8), N = x (8), K = row parity x 16 columns
+            const int32_t two[4] = {2, 2, 2, 2};
 #pragma unroll
-        for (int n = 0; n < NU; ++n)
-            load4<F, 1>(t < 2 ? boxU[n] : boxU[n] + F::ST_C, ubC[n], g, t & 1, hvC, wvC, XPART, blo[n], bhi[n]);
+            for (int n = 0; n < NU; ++n) {
+                const int ub0 = ubC[n] * F::RB_C;
+                const int r0 = min(2 * g, hvC - 1), r1 = min(2 * g + 1, hvC - 1);
+                uint32_t A[4];
+                A[0] = lds32(boxU[n] + swz<F::IB_C>(r0 * F::IB_C + ub0 + 4 * t));
+                A[1] = lds32(boxU[n] + F::ST_C + swz<F::IB_C>(r0 * F::IB_C + ub0 + 4 * t));
+                A[2] = lds32(boxU[n] + swz<F::IB_C>(r1 * F::IB_C + ub0 + 4 * t));
+                A[3] = lds32(boxU[n] + F::ST_C + swz<F::IB_C>(r1 * F::IB_C + ub0 + 4 * t));
+                int32_t S[4];
+                mma32_uu_acc(S, A, L.rc, L.rc, two);
+                // slots 4t+i: U x = 2t + i (i < 2), V x = 2t + i - 2 -> the p8 permutation
+                blo[n] = pack_ds(S[0], S[1], S[2], S[3]);
+                bhi[n] = 0;
+            }
+        } else {
+#pragma unroll
+            for (int n = 0; n < NU; ++n)
+                load4<F, 1>(t < 2 ? boxU[n] : boxU[n] + F::ST_C, ubC[n], g, t & 1, hvC, wvC, XPART, blo[n], bhi[n]);
+        }
         int32_t C[NU][4];
 #pragma unroll
-        for (int n = 0; n < NU; ++n) dct8pair<ES>(L, blo[n], bhi[n], C[n]);
+        for (int n = 0; n < NU; ++n) dct8pair<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
-            o[n].hu = fma(U.wc[1], fabs(__int2double_rn(C[n][1])), U.wc[0] * fabs(__int2double_rn(C[n][0])));
-            o[n].hv = fma(U.wc[1], fabs(__int2double_rn(C[n][3])), U.wc[0] * fabs(__int2double_rn(C[n][2])));
+            o[n].hu = fma(VCA_WC(1), fabs(__int2double_rn(C[n][1])), VCA_WC(0) * fabs(__int2double_rn(C[n][0])));
+            o[n].hv = fma(VCA_WC(1), fabs(__int2double_rn(C[n][3])), VCA_WC(0) * fabs(__int2double_rn(C[n][2])));
             o[n].dcU = C[n][0];
             o[n].dcV = C[n][2];
             if (DUMP) {
@@ -760,6 +878,18 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
             U.wc[e] = NC == 16 ? U.wl16[e] : __ldg(W8 + g * 8 + 2 * t + e);
     }
     U.wtab = wtab + lane;
+    {
+        // [e][lane] weight table (same values as the registers; filled by consumer warp 0)
+        const uint32_t wsm0 = smem_u32(stash) + 4 * F::STASH;
+        if (u == 0) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) sts_f64(wsm0 + (e * 32 + lane) * 8, U.wl16[e]);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) sts_f64(wsm0 + ((8 + e) * 32 + lane) * 8, NC == 8 ? U.wc[e] : 0.0);
+        }
+        U.wsm = wsm0 + lane * 8;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // consumer warps only
+    }
     U.g = g;
     U.t = t;
     const double invNY = 1.0 / NY, invNC = 1.0 / NC;
