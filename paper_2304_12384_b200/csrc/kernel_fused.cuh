@@ -80,23 +80,28 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+#ifdef VCA_MMA_NONVOLATILE
+#define VCA_MMA_ASM asm  // pure register op: lets the compiler reorder around it
+#else
+#define VCA_MMA_ASM asm volatile
+#endif
 // D = A(s8) . B(u8) + C, m16n8k16
 __device__ __forceinline__ void mma16_su(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b)
 {
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
+    VCA_MMA_ASM("mma.sync.aligned.m16n8k16.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
                  : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
                  : "r"(a0), "r"(a1), "r"(b), "r"(0), "r"(0), "r"(0), "r"(0));
 }
 __device__ __forceinline__ void mma16_ss(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b)
 {
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
+    VCA_MMA_ASM("mma.sync.aligned.m16n8k16.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
                  : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
                  : "r"(a0), "r"(a1), "r"(b), "r"(0), "r"(0), "r"(0), "r"(0));
 }
 // m16n8k32
 __device__ __forceinline__ void mma32_su(int32_t (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
 {
-    asm volatile(
+    VCA_MMA_ASM(
         "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%10,%11,%12,%13};"
         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
@@ -104,7 +109,7 @@ __device__ __forceinline__ void mma32_su(int32_t (&d)[4], const uint32_t (&a)[4]
 }
 __device__ __forceinline__ void mma32_ss(int32_t (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1)
 {
-    asm volatile(
+    VCA_MMA_ASM(
         "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%10,%11,%12,%13};"
         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
@@ -209,6 +214,17 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t a)
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
 }
+#ifndef VCA_ASMLOADS
+// C++ loads through the dynamic-smem array: the compiler knows the shared address space
+// (LDS) and may schedule them freely after the (volatile, memory-clobbering) barrier wait.
+extern __shared__ __align__(1024) uint8_t vca_dyn_smem[];
+__device__ __forceinline__ const uint8_t *smem_ptr(uint32_t a)
+{
+    return vca_dyn_smem + (a - (uint32_t)__cvta_generic_to_shared(vca_dyn_smem));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) { return *reinterpret_cast<const uint32_t *>(smem_ptr(a)); }
+__device__ __forceinline__ uint2 lds64(uint32_t a) { return *reinterpret_cast<const uint2 *>(smem_ptr(a)); }
+#else
 __device__ __forceinline__ uint32_t lds32(uint32_t a)
 {
     uint32_t v;
@@ -221,6 +237,7 @@ __device__ __forceinline__ uint2 lds64(uint32_t a)
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
+#endif
 __device__ __forceinline__ double lds_f64(uint32_t a)
 {
     double v;
@@ -235,12 +252,16 @@ __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
 {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+#ifndef VCA_ASMLOADS
+__device__ __forceinline__ uint4 lds128(uint32_t a) { return *reinterpret_cast<const uint4 *>(smem_ptr(a)); }
+#else
 __device__ __forceinline__ uint4 lds128(uint32_t a)
 {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
     return v;
 }
+#endif
 
 // One sample of a unit in a swizzled box (row, column within the unit), 10-bit clamp
 template <int ES, int IB>
@@ -257,10 +278,20 @@ __device__ __forceinline__ int box_sample(uint32_t box, int ub0, int row, int xs
 // picks byte 0 of each lane after >> 2 (s >> 2 <= 255, so no masking is needed).
 __device__ __forceinline__ uint32_t ds8(uint2 a, uint2 b)
 {
+#ifndef VCA_DS_ALU
+    // 2x2 sums as byte dot products on the FMA pipe (IDP.4A) with weights 64: s' = 64 (s + 2)
+    // < 2^16, so byte 1 of s' is (s + 2) >> 2 and three PRMTs pack the four outputs
+    const uint32_t s0 = __dp4a(a.x, 0x00004040u, __dp4a(b.x, 0x00004040u, 128u));
+    const uint32_t s1 = __dp4a(a.x, 0x40400000u, __dp4a(b.x, 0x40400000u, 128u));
+    const uint32_t s2 = __dp4a(a.y, 0x00004040u, __dp4a(b.y, 0x00004040u, 128u));
+    const uint32_t s3 = __dp4a(a.y, 0x40400000u, __dp4a(b.y, 0x40400000u, 128u));
+    return __byte_perm(__byte_perm(s0, s1, 0x0051), __byte_perm(s2, s3, 0x0051), 0x5410);
+#else
     const uint32_t M = 0x00FF00FFu;
     const uint32_t sl = (a.x & M) + __byte_perm(a.x, 0u, 0x4341) + (b.x & M) + __byte_perm(b.x, 0u, 0x4341) + 0x00020002u;
     const uint32_t sh = (a.y & M) + __byte_perm(a.y, 0u, 0x4341) + (b.y & M) + __byte_perm(b.y, 0u, 0x4341) + 0x00020002u;
     return __byte_perm(sl >> 2, sh >> 2, 0x6420);
+#endif
 }
 
 // four (2x2 sum + 2) values < 1024 -> packed bytes (s >> 2): low halves paired by PRMT,
@@ -785,7 +816,11 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
 {
     using F = Fam<W_, BD_, LP_>;
     constexpr int NY = F::NY, NC = F::NC, W = F::W, WC = F::WC, NU = F::NU;
+#ifndef VCA_ASMLOADS
+    uint8_t *smem_raw = vca_dyn_smem;
+#else
     extern __shared__ uint8_t smem_raw[];
+#endif
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + F::STAGES * F::STAGE);
     uint64_t *empty = full + F::STAGES;
