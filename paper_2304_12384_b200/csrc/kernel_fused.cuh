@@ -557,11 +557,18 @@ constexpr bool kMmaDownsample = true;   // A/B: 2x2 low-pass sums as a 0/1 IMMA 
 constexpr bool kMmaDownsample = false;
 #endif
 
+#ifndef VCA_NO_ACC_CHROMA
+constexpr bool kAccChroma = true;  // chroma |C| FMAs go straight into the running sums (+2 %)
+#else
+constexpr bool kAccChroma = false;
+#endif
+
 template <class F, bool XPART, bool DUMP, int NU>
 __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedArgs &a, const uint32_t (&boxY)[NU],
                                               const uint32_t (&boxU)[NU], const int (&ubY)[NU],
                                               const int (&ubC)[NU], int hvY, int hvC, int wvY, int wvC,
-                                              const int64_t (&k)[NU], UnitOut (&o)[NU])
+                                              const int64_t (&k)[NU], UnitOut (&o)[NU], double &hu_acc,
+                                              double &hv_acc)
 {
     constexpr int NY = F::NY, NC = F::NC, ES = F::ES;
     const int g = U.g, t = U.t;
@@ -632,6 +639,12 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             // |C| folds into the DFMA operand (fabs of an exact int32 -> double conversion)
+#ifdef VCA_SINGLE_CHAIN
+            double h0 = 0.0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) h0 = fma(VCA_WL(e), fabs(__int2double_rn(C[n][e >> 2][e & 3])), h0);
+            hY[n] = h0;
+#else
             double h0 = 0.0, h1 = 0.0;  // two FMA chains, combined once (fixed order)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -639,6 +652,7 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                 h1 = fma(VCA_WL(4 + e), fabs(__int2double_rn(C[n][1][e])), h1);
             }
             hY[n] = h0 + h1;
+#endif
             o[n].dcY = C[n][0][0];
             if (DUMP) {
 #pragma unroll
@@ -734,8 +748,16 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
         for (int n = 0; n < NU; ++n) dct8pair<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
-            o[n].hu = fma(VCA_WC(1), fabs(__int2double_rn(C[n][1])), VCA_WC(0) * fabs(__int2double_rn(C[n][0])));
-            o[n].hv = fma(VCA_WC(1), fabs(__int2double_rn(C[n][3])), VCA_WC(0) * fabs(__int2double_rn(C[n][2])));
+            if (kAccChroma && !DUMP) {
+                // straight into the warp's running U/V sums (unit order, fixed)
+                hu_acc = fma(VCA_WC(1), fabs(__int2double_rn(C[n][1])), fma(VCA_WC(0), fabs(__int2double_rn(C[n][0])), hu_acc));
+                hv_acc = fma(VCA_WC(1), fabs(__int2double_rn(C[n][3])), fma(VCA_WC(0), fabs(__int2double_rn(C[n][2])), hv_acc));
+            } else {
+                o[n].hu = fma(VCA_WC(1), fabs(__int2double_rn(C[n][1])), VCA_WC(0) * fabs(__int2double_rn(C[n][0])));
+                o[n].hv = fma(VCA_WC(1), fabs(__int2double_rn(C[n][3])), VCA_WC(0) * fabs(__int2double_rn(C[n][2])));
+                hu_acc += o[n].hu;
+                hv_acc += o[n].hv;
+            }
             o[n].dcU = C[n][0];
             o[n].dcV = C[n][2];
             if (DUMP) {
@@ -763,9 +785,11 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             if (pl == 1) {
                 o[0].hu = hacc;
                 o[0].dcU = C[0][0];
+                hu_acc += hacc;
             } else {
                 o[0].hv = hacc;
                 o[0].dcV = C[0][0];
+                hv_acc += hacc;
             }
             if (DUMP) {
 #pragma unroll
@@ -963,7 +987,7 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
                     kk[n] = (int64_t)r * cols + c0 + 4 * n;
                     valid[n] = true;
                 }
-                process_units<F, false, DUMP, NU>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o);
+                process_units<F, false, DUMP, NU>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o, hu, hv);
             } else {
                 // ragged strip end or a partial last block column: one unit at a time
 #pragma unroll
@@ -979,9 +1003,9 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
                     const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
                     UnitOut o1[1];
                     if (wvY < W)
-                        process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1);
+                        process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1, hu, hv);
                     else
-                        process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1);
+                        process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1, hu, hv);
                     o[n] = o1[0];
                 }
             }
@@ -989,8 +1013,6 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
             for (int n = 0; n < NU; ++n) {
                 if (!valid[n]) continue;
                 const int slot = (s * NU + n) & 31;
-                hu += o[n].hu;
-                hv += o[n].hv;
                 // stash: per-unit luma row-group partials and DC sums, reduced 32 units at a time
                 if (t == 0) sts_f64(hst + (slot * 9 + g) * 8, o[n].hY);
                 if (lane == 0) {
