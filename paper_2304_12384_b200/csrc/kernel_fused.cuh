@@ -248,6 +248,10 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double v)
 {
     asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
+__device__ __forceinline__ void sts_v3u32(uint32_t a, uint32_t x, uint32_t y, uint32_t z)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(0u) : "memory");
+}
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
 {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -956,6 +960,23 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
     const uint32_t full0 = smem_u32(full);
     const int64_t CY = (int64_t)rows * cols;
 
+    // per-warp constants: smem offsets of this warp's units inside a stage, and the number of
+    // leading strips in which all NU units of this warp are whole (valid, not a partial
+    // last block column) -- those take the NU-wide fast path
+    uint32_t offY[NU], offU[NU];
+    int ubYc[NU], ubCc[NU];
+#pragma unroll
+    for (int n = 0; n < NU; ++n) {
+        const int v = u + 4 * n;
+        offY[n] = (v / F::UPB_Y) * F::BOXB_Y;
+        offU[n] = F::ST_Y + (v / F::UPB_C) * F::BOXB_C;
+        ubYc[n] = v % F::UPB_Y;
+        ubCc[n] = v % F::UPB_C;
+    }
+    const int cols_whole = (a.width[0] % W) ? cols - 1 : cols;
+    const int last_c = u + 4 * (NU - 1);  // c of this warp's last unit in strip 0
+    const int s_fast = cols_whole > last_c ? (cols_whole - last_c - 1) / F::UNITS + 1 : 0;
+
     uint32_t st = 0, phase = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int f = it / rows, r = it - f * rows;
@@ -970,24 +991,19 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
             const uint32_t base = smem0 + st * F::STAGE;
             const int c0 = s * F::UNITS + u;
 #ifndef VCA_NULL_COMPUTE
-            const bool full_group = c0 + 4 * (NU - 1) < cols && a.width[0] - (c0 + 4 * (NU - 1)) * W >= W;
             UnitOut o[NU];
             bool valid[NU];
-            if (full_group) {
+            if (s < s_fast) {
                 uint32_t bY[NU], bU[NU];
-                int uY[NU], uC[NU];
                 int64_t kk[NU];
 #pragma unroll
                 for (int n = 0; n < NU; ++n) {
-                    const int v = u + 4 * n;  // unit index within the strip
-                    bY[n] = base + (v / F::UPB_Y) * F::BOXB_Y;
-                    bU[n] = base + F::ST_Y + (v / F::UPB_C) * F::BOXB_C;
-                    uY[n] = v % F::UPB_Y;
-                    uC[n] = v % F::UPB_C;
-                    kk[n] = (int64_t)r * cols + c0 + 4 * n;
+                    bY[n] = base + offY[n];
+                    bU[n] = base + offU[n];
+                    kk[n] = DUMP ? (int64_t)r * cols + c0 + 4 * n : 0;
                     valid[n] = true;
                 }
-                process_units<F, false, DUMP, NU>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o, hu, hv);
+                process_units<F, false, DUMP, NU>(U, a, bY, bU, ubYc, ubCc, hvY, hvC, W, WC, kk, o, hu, hv);
             } else {
                 // ragged strip end or a partial last block column: one unit at a time
 #pragma unroll
@@ -1015,12 +1031,9 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
                 const int slot = (s * NU + n) & 31;
                 // stash: per-unit luma row-group partials and DC sums, reduced 32 units at a time
                 if (t == 0) sts_f64(hst + (slot * 9 + g) * 8, o[n].hY);
-                if (lane == 0) {
-                    // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
-                    sts_u32(sxs + slot * 16 + 0, (uint32_t)o[n].dcY >> 12);
-                    sts_u32(sxs + slot * 16 + 4, (uint32_t)o[n].dcU >> 12);
-                    sts_u32(sxs + slot * 16 + 8, (uint32_t)o[n].dcV >> 12);
-                }
+                if (lane == 0)  // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
+                    sts_v3u32(sxs + slot * 16, (uint32_t)o[n].dcY >> 12, (uint32_t)o[n].dcU >> 12,
+                              (uint32_t)o[n].dcV >> 12);
             }
 #endif
             __syncwarp();
