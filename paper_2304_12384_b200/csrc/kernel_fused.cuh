@@ -35,6 +35,13 @@
 
 namespace vca {
 
+// A/B (tools/ab_variants.py, 600 frames): G = 3 groups with 152-register consumers and
+// NU = 4 units per warp per strip: config 3 400k -> 432k fps, config 2 545k -> 565k, config 4
+// flat; G = 4 (104 registers) or G = 2 (8 consumer warps) are slower.
+#ifndef VCA_GROUPS
+#define VCA_GROUPS 3
+#endif
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -151,6 +158,20 @@ __device__ __forceinline__ double abs_to_double(int32_t c)
 #endif
 }
 
+// Exact double of an int32 without the conversion pipe (I2F.F64 retires 16 lanes/clk/SM on
+// B200, DADD 64; tools/micro/pipes.cu): with M = 2^52 + 2^51, the double M + c has low word c
+// and high word 0x43380000 + (c >> 31) (one LEA.HI.SX32), and (M + c) - M = c exactly (DADD).
+// A/B (config 2/3/4): I2F.F64 is faster overall -- the kernel is issue-bound, not XU-bound,
+// and the magic form costs an extra instruction -- so it is the default.
+__device__ __forceinline__ double i2d(int32_t c)
+{
+#ifndef VCA_CVT_MAGIC
+    return __int2double_rn(c);
+#else
+    return __hiloint2double(0x43380000 + (c >> 31), c) - 6755399441055744.0;
+#endif
+}
+
 __device__ __forceinline__ int32_t combine3(int32_t d0, int32_t d1, int32_t d2)
 {
     return (int32_t)((uint32_t)d0 + ((uint32_t)d1 << 8) + ((uint32_t)d2 << 16));
@@ -164,9 +185,11 @@ struct Fam {
     static constexpr int NY = LP ? W / 2 : W;
     static constexpr int NC = LP ? WC / 2 : WC;
 #ifndef VCA_NU
-#define VCA_NU 2
+#define VCA_NU (VCA_GROUPS == 3 ? 4 : 2)
 #endif
-    static constexpr int NU = (NY == 16) ? VCA_NU : 1;     // units per consumer warp per strip (ILP)
+    // units per consumer warp per strip (ILP, per-strip overhead); 4 only while a 16-unit stage
+    // stays <= 24 KB (two stages per group, three groups per CTA)
+    static constexpr int NU = (NY != 16) ? 1 : (VCA_NU == 4 && 24 * ES * W * W > 24576) ? 2 : VCA_NU;
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
     static constexpr int IB_Y = (UNITS * RB_Y) < 128 ? UNITS * RB_Y : 128;  // box inner bytes = swizzle span
@@ -540,7 +563,7 @@ struct UnitCtx {
     LaneConst L;
     double wl16[8];     // luma n = 16 weights at this lane's 8 positions
     double wc[NWC];     // chroma weights at this lane's positions
-    const double *wtab; // luma n = 32 weights in smem, [slot][lane] + lane
+    uint32_t wtab;      // smem address of this lane's luma n = 32 weights ([slot][lane] doubles)
     uint32_t wsm;       // smem address of this lane's n = 16 / 8 weights ([e][lane])
     int g, t;
 };
@@ -561,6 +584,24 @@ constexpr bool kMmaDownsample = true;   // A/B: 2x2 low-pass sums as a 0/1 IMMA 
 constexpr bool kMmaDownsample = false;
 #endif
 
+// Chroma needs only per-frame sums (A7), so a lane may add |C| per coefficient position into
+// exact uint32 accumulators and apply the weight once per flush (every FC units; FC keeps
+// the sums below 2^32: |C| <= (64 n)^2 (2^bd - 1) and FC * that < 2^32) -- no conversion or
+// FP64 op per chroma coefficient, exact sums, only the flushes round.  A/B: +2 % for the
+// n = 16 chroma of the full 32x32 path (16 positions per lane), -2..-5 % for n = 8 chroma
+// (2 positions per lane; the IABS/IADD land on the busiest ALU pipe), so n = 16 only.
+#ifndef VCA_INT_CHROMA
+#define VCA_INT_CHROMA 1  // 0 never, 1 n = 16 chroma only, 2 always
+#endif
+
+template <class F>
+struct ChromaAcc {
+    static constexpr bool ON = VCA_INT_CHROMA == 2 || (VCA_INT_CHROMA == 1 && F::NC == 16);
+    static constexpr int NP = F::NC == 16 ? 8 : 2;  // coefficient positions per lane per plane
+    static constexpr int FC = (F::NC == 16 && F::ES == 2) ? 4 : 16;  // units per flush
+    uint32_t u[NP], v[NP];
+};
+
 #ifndef VCA_NO_ACC_CHROMA
 constexpr bool kAccChroma = true;  // chroma |C| FMAs go straight into the running sums (+2 %)
 #else
@@ -572,7 +613,7 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                                               const uint32_t (&boxU)[NU], const int (&ubY)[NU],
                                               const int (&ubC)[NU], int hvY, int hvC, int wvY, int wvC,
                                               const int64_t (&k)[NU], UnitOut (&o)[NU], double &hu_acc,
-                                              double &hv_acc)
+                                              double &hv_acc, ChromaAcc<F> &ca)
 {
     constexpr int NY = F::NY, NC = F::NC, ES = F::ES;
     const int g = U.g, t = U.t;
@@ -646,14 +687,14 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 #ifdef VCA_SINGLE_CHAIN
             double h0 = 0.0;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) h0 = fma(VCA_WL(e), fabs(__int2double_rn(C[n][e >> 2][e & 3])), h0);
+            for (int e = 0; e < 8; ++e) h0 = fma(VCA_WL(e), fabs(i2d(C[n][e >> 2][e & 3])), h0);
             hY[n] = h0;
 #else
             double h0 = 0.0, h1 = 0.0;  // two FMA chains, combined once (fixed order)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                h0 = fma(VCA_WL(e), fabs(__int2double_rn(C[n][0][e])), h0);
-                h1 = fma(VCA_WL(4 + e), fabs(__int2double_rn(C[n][1][e])), h1);
+                h0 = fma(VCA_WL(e), fabs(i2d(C[n][0][e])), h0);
+                h1 = fma(VCA_WL(4 + e), fabs(i2d(C[n][1][e])), h1);
             }
             hY[n] = h0 + h1;
 #endif
@@ -704,7 +745,7 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int32_t cc = combine3(E0[e], E1[e], E2[e]);
-                    hacc = fma(U.wtab[((mt * 4 + rr) * 4 + e) * 32], fabs(__int2double_rn(cc)), hacc);
+                    hacc = fma(lds_f64(U.wtab + ((mt * 4 + rr) * 4 + e) * 32 * 8), fabs(i2d(cc)), hacc);
                     if (mt == 0 && rr == 0 && e == 0) o[0].dcY = cc;
                     if (DUMP)
                         a.dump.coeffs[0][k[0] * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
@@ -752,13 +793,22 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
         for (int n = 0; n < NU; ++n) dct8pair<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
-            if (kAccChroma && !DUMP) {
+            if (ChromaAcc<F>::ON) {
+                ca.u[0] += (uint32_t)abs(C[n][0]);
+                ca.u[1] += (uint32_t)abs(C[n][1]);
+                ca.v[0] += (uint32_t)abs(C[n][2]);
+                ca.v[1] += (uint32_t)abs(C[n][3]);
+                if (DUMP) {
+                    o[n].hu = fma(VCA_WC(1), fabs(i2d(C[n][1])), VCA_WC(0) * fabs(i2d(C[n][0])));
+                    o[n].hv = fma(VCA_WC(1), fabs(i2d(C[n][3])), VCA_WC(0) * fabs(i2d(C[n][2])));
+                }
+            } else if (kAccChroma && !DUMP) {
                 // straight into the warp's running U/V sums (unit order, fixed)
-                hu_acc = fma(VCA_WC(1), fabs(__int2double_rn(C[n][1])), fma(VCA_WC(0), fabs(__int2double_rn(C[n][0])), hu_acc));
-                hv_acc = fma(VCA_WC(1), fabs(__int2double_rn(C[n][3])), fma(VCA_WC(0), fabs(__int2double_rn(C[n][2])), hv_acc));
+                hu_acc = fma(VCA_WC(1), fabs(i2d(C[n][1])), fma(VCA_WC(0), fabs(i2d(C[n][0])), hu_acc));
+                hv_acc = fma(VCA_WC(1), fabs(i2d(C[n][3])), fma(VCA_WC(0), fabs(i2d(C[n][2])), hv_acc));
             } else {
-                o[n].hu = fma(VCA_WC(1), fabs(__int2double_rn(C[n][1])), VCA_WC(0) * fabs(__int2double_rn(C[n][0])));
-                o[n].hv = fma(VCA_WC(1), fabs(__int2double_rn(C[n][3])), VCA_WC(0) * fabs(__int2double_rn(C[n][2])));
+                o[n].hu = fma(VCA_WC(1), fabs(i2d(C[n][1])), VCA_WC(0) * fabs(i2d(C[n][0])));
+                o[n].hv = fma(VCA_WC(1), fabs(i2d(C[n][3])), VCA_WC(0) * fabs(i2d(C[n][2])));
                 hu_acc += o[n].hu;
                 hv_acc += o[n].hv;
             }
@@ -782,18 +832,31 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             int32_t C[2][4];
             dct16<ES>(L, blo, bhi, C);
             double hacc = 0.0;
+            if (ChromaAcc<F>::ON) {
 #pragma unroll
-            for (int p = 0; p < 2; ++p)
+                for (int p = 0; p < 2; ++p)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) hacc = fma(U.wc[p * 4 + e], fabs(__int2double_rn(C[p][e])), hacc);
+                    for (int e = 0; e < 4; ++e) {
+                        if (pl == 1)
+                            ca.u[p * 4 + e] += (uint32_t)abs(C[p][e]);
+                        else
+                            ca.v[p * 4 + e] += (uint32_t)abs(C[p][e]);
+                    }
+            }
+            if (!ChromaAcc<F>::ON || DUMP) {
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) hacc = fma(U.wc[p * 4 + e], fabs(i2d(C[p][e])), hacc);
+            }
             if (pl == 1) {
                 o[0].hu = hacc;
                 o[0].dcU = C[0][0];
-                hu_acc += hacc;
+                if (!ChromaAcc<F>::ON) hu_acc += hacc;
             } else {
                 o[0].hv = hacc;
                 o[0].dcV = C[0][0];
-                hv_acc += hacc;
+                if (!ChromaAcc<F>::ON) hv_acc += hacc;
             }
             if (DUMP) {
 #pragma unroll
@@ -833,12 +896,36 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     }
 }
 
-constexpr int kFusedThreads = 160;  // producer warp + 4 consumer warps (A/B: a producer-less
-constexpr int kConsumer0 = 1;       // ring refilled by the last releasing warp lost 16 %)
+// CTA layouts.
+//  * kGroups == 0: 160 threads = 1 producer warp + 4 consumer warps (A/B: a producer-less
+//    ring refilled by the last releasing warp lost 16 %), MINB CTAs per SM.
+//  * kGroups == G > 0: warp-specialised with register reallocation, 1 CTA per SM:
+//    warpgroup 0 = producers (warp g < G feeds group g; setmaxnreg.dec to VCA_PREG),
+//    warpgroups 1..G = consumer groups of 4 warps (setmaxnreg.inc to VCA_CREG), each group
+//    with its own ring, walking its own item sequence exactly like one legacy CTA.
+#ifndef VCA_PREG
+#define VCA_PREG 40  // producer warpgroup (24 spills the producer loop)
+#endif
+#ifndef VCA_CREG
+#define VCA_CREG (VCA_GROUPS == 2 ? 232 : VCA_GROUPS == 3 ? 152 : 104)  // 65536 / threads + released
+#endif
+constexpr int kGroups = VCA_GROUPS;
+constexpr int kGv = kGroups ? kGroups : 1;  // consumer groups per CTA
+constexpr int kFusedThreads = kGroups ? 128 * (1 + kGroups) : 160;
 constexpr int kConsumers = 4;
 
+template <class F>
+struct Lay {  // shared-memory layout (offsets from the 1024-aligned base)
+    static constexpr int GRP = (F::STAGES * F::STAGE + 2 * F::STAGES * 8 + 1023) / 1024 * 1024;  // ring + bars
+    static constexpr int WTAB_OFF = kGv * GRP;
+    static constexpr int STASH_OFF = WTAB_OFF + (F::WTAB ? 32 * 32 * 8 : 0);
+    static constexpr int WSM_OFF = STASH_OFF + 4 * kGv * F::STASH;
+    static constexpr int SMEM = 1024 + WSM_OFF + kGv * 10 * 32 * 8;
+    static_assert(SMEM <= 232448, "dynamic shared memory over the 227 KB per-CTA limit");
+};
+
 template <int W_, int BD_, int LP_, bool DUMP>
-__global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
+__global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>::MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
                                                     const __grid_constant__ CUtensorMap tmU,
                                                     const __grid_constant__ CUtensorMap tmV, const FusedArgs a)
 {
@@ -849,18 +936,26 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
 #else
     extern __shared__ uint8_t smem_raw[];
 #endif
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + F::STAGES * F::STAGE);
-    uint64_t *empty = full + F::STAGES;
-    double *wtab = reinterpret_cast<double *>(empty + F::STAGES);
+    using Y = Lay<F>;
+    uint8_t *smem0p = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    double *wtab = reinterpret_cast<double *>(smem0p + Y::WTAB_OFF);
     // per consumer warp: hst[32 slots][9] (8 row-group partials, padded) + sxs[32][4] DC sums
-    uint8_t *stash = reinterpret_cast<uint8_t *>(wtab + (F::WTAB ? 32 * 32 : 0));
+    uint8_t *stash = smem0p + Y::STASH_OFF;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // consumer group of this warp (producer warp g < kGroups feeds group g)
+    const int grp = kGroups ? (warp < 4 ? warp : (warp >> 2) - 1) : 0;
+    uint8_t *smem = smem0p + (grp < kGv ? grp : 0) * Y::GRP;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + F::STAGES * F::STAGE);
+    uint64_t *empty = full + F::STAGES;
+    const int vblk = blockIdx.x * kGv + grp, vgrid = gridDim.x * kGv;  // virtual CTA of the group
     if (threadIdx.x == 0) {
-        for (int i = 0; i < F::STAGES; ++i) {
-            mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumers);
+        for (int q = 0; q < kGv; ++q) {
+            uint64_t *fq = reinterpret_cast<uint64_t *>(smem0p + q * Y::GRP + F::STAGES * F::STAGE);
+            for (int i = 0; i < F::STAGES; ++i) {
+                mbar_init(&fq[i], 1);
+                mbar_init(&fq[F::STAGES + i], kConsumers);
+            }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -881,9 +976,12 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
     const int strips = (cols + F::UNITS - 1) / F::UNITS;
     const int items = a.n_frames * rows;  // < 2^31 (checked on the host)
 
-    if (warp == 0) {
+    if (kGroups ? warp < 4 : warp == 0) {
         // ---------------- TMA producer (A1)
-        if (lane == 0) {
+#if VCA_GROUPS
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VCA_PREG));
+#endif
+        if (lane == 0 && warp < kGv) {
             uint64_t policy;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmY)) : "memory");
@@ -891,7 +989,7 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
             uint32_t st = 0, phase = 0;
             bool first_pass = true;
-            for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            for (int it = vblk; it < items; it += vgrid) {
                 const int f = it / rows, r = it - f * rows;
                 for (int s = 0; s < strips; ++s) {
                     if (!first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
@@ -920,9 +1018,12 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
     }
 
     // ---------------- consumers
-    const int u = warp - kConsumer0;
+#if VCA_GROUPS
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VCA_CREG));
+#endif
+    const int u = kGroups ? (warp & 3) : warp - 1;
     const int g = lane >> 2, t = lane & 3;
-    const uint32_t hst = smem_u32(stash) + u * F::STASH;  // [32][9] doubles
+    const uint32_t hst = smem_u32(stash) + (grp * 4 + u) * F::STASH;  // [32][9] doubles
     const uint32_t sxs = hst + 32 * 9 * 8;                 // [32][4] uint32
     UnitCtx<F> U;
     build_lane_const(U.L, a.T_all, g, t, NY);
@@ -940,10 +1041,10 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
         for (int e = 0; e < UnitCtx<F>::NWC; ++e)
             U.wc[e] = NC == 16 ? U.wl16[e] : __ldg(W8 + g * 8 + 2 * t + e);
     }
-    U.wtab = wtab + lane;
+    U.wtab = smem_u32(wtab) + lane * 8;
     {
         // [e][lane] weight table (same values as the registers; filled by consumer warp 0)
-        const uint32_t wsm0 = smem_u32(stash) + 4 * F::STASH;
+        const uint32_t wsm0 = smem_u32(smem0p + Y::WSM_OFF) + grp * 10 * 32 * 8;
         if (u == 0) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) sts_f64(wsm0 + (e * 32 + lane) * 8, U.wl16[e]);
@@ -951,7 +1052,7 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
             for (int e = 0; e < 2; ++e) sts_f64(wsm0 + ((8 + e) * 32 + lane) * 8, NC == 8 ? U.wc[e] : 0.0);
         }
         U.wsm = wsm0 + lane * 8;
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // consumer warps only
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");  // this group's consumer warps
     }
     U.g = g;
     U.t = t;
@@ -978,10 +1079,13 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
     const int s_fast = cols_whole > last_c ? (cols_whole - last_c - 1) / F::UNITS + 1 : 0;
 
     uint32_t st = 0, phase = 0;
-    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    for (int it = vblk; it < items; it += vgrid) {
         const int f = it / rows, r = it - f * rows;
         const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
         double hu = 0.0, hv = 0.0;                          // per-lane U/V texture partials (fixed order)
+        ChromaAcc<F> ca;                                    // exact per-position chroma |C| sums
+#pragma unroll
+        for (int e = 0; e < ChromaAcc<F>::NP; ++e) ca.u[e] = ca.v[e] = 0u;
         double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // identical in all lanes
         double *HYrow = a.s.HY + (int64_t)f * CY + (int64_t)r * cols;
         for (int s = 0; s < strips; ++s) {
@@ -1003,7 +1107,7 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
                     kk[n] = DUMP ? (int64_t)r * cols + c0 + 4 * n : 0;
                     valid[n] = true;
                 }
-                process_units<F, false, DUMP, NU>(U, a, bY, bU, ubYc, ubCc, hvY, hvC, W, WC, kk, o, hu, hv);
+                process_units<F, false, DUMP, NU>(U, a, bY, bU, ubYc, ubCc, hvY, hvC, W, WC, kk, o, hu, hv, ca);
             } else {
                 // ragged strip end or a partial last block column: one unit at a time
 #pragma unroll
@@ -1019,9 +1123,9 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
                     const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
                     UnitOut o1[1];
                     if (wvY < W)
-                        process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1, hu, hv);
+                        process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1, hu, hv, ca);
                     else
-                        process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1, hu, hv);
+                        process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1, hu, hv, ca);
                     o[n] = o1[0];
                 }
             }
@@ -1043,6 +1147,15 @@ __global__ void __launch_bounds__(kFusedThreads, Fam<W_, BD_, LP_>::MINB) fused_
                 phase ^= 1;
             }
             const int mlast = s * NU + NU - 1;  // last unit index of this strip
+            if (ChromaAcc<F>::ON && (((mlast + 1) % ChromaAcc<F>::FC) == 0 || s == strips - 1)) {
+                // chroma flush: weight the exact per-position sums once (fixed position order)
+#pragma unroll
+                for (int e = 0; e < ChromaAcc<F>::NP; ++e) {
+                    hu = fma(U.wc[e], __uint2double_rn(ca.u[e]), hu);
+                    hv = fma(U.wc[e], __uint2double_rn(ca.v[e]), hv);
+                    ca.u[e] = ca.v[e] = 0u;
+                }
+            }
             if ((mlast & 31) == 31 || s == strips - 1) {
                 // flush: lane l finishes unit m = mlast - (mlast & 31) + l -- H_Y (fixed order
                 // over the 8 row groups), its L terms (A6), the per-block H_Y store (A5, needed
@@ -1139,9 +1252,9 @@ inline cudaError_t prepare_one()
 {
     using F = Fam<W, BD, LP>;
     cudaError_t e = cudaFuncSetAttribute(fused_kernel<W, BD, LP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         F::SMEM);
+                                         Lay<F>::SMEM);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(fused_kernel<W, BD, LP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM);
+        e = cudaFuncSetAttribute(fused_kernel<W, BD, LP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay<F>::SMEM);
     return e;
 }
 
@@ -1177,14 +1290,14 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     const bool dump = dp.coeffs[0] != nullptr;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
     int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, F::SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, Lay<F>::SMEM) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     const int64_t items = (int64_t)n_frames * a.rows;
     if (items > 0x7fffffff) return -2;
     int64_t grid = (int64_t)sm_count * per_sm;
     if (grid > items) grid = items;
-    kern<<<(unsigned)grid, kFusedThreads, F::SMEM, st>>>(mY, mU, mV, a);
+    kern<<<(unsigned)grid, kFusedThreads, Lay<F>::SMEM, st>>>(mY, mU, mV, a);
     return 0;
 }
 
