@@ -225,70 +225,32 @@ __device__ __forceinline__ uint32_t swz(uint32_t off)
     return off ^ (((off >> 7) & m) << 4);
 }
 
-__device__ __forceinline__ uint32_t lds_u8(uint32_t a)
-{
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ uint32_t lds_u16(uint32_t a)
-{
-    uint16_t v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-    return v;
-}
-#ifndef VCA_ASMLOADS
-// C++ loads through the dynamic-smem array: the compiler knows the shared address space
-// (LDS) and may schedule them freely after the (volatile, memory-clobbering) barrier wait.
+// Data-path shared-memory accesses take byte OFFSETS into the dynamic shared array and are
+// plain C++ loads/stores: the compiler knows the address space (LDS/STS with immediate
+// offsets, no generic-window arithmetic) and schedules them freely between the volatile,
+// memory-clobbering mbarrier wait and arrive.  Barriers and TMA take shared addresses
+// (smem_u32).
 extern __shared__ __align__(1024) uint8_t vca_dyn_smem[];
-__device__ __forceinline__ const uint8_t *smem_ptr(uint32_t a)
+__device__ __forceinline__ uint32_t smem_off(const void *p)
 {
-    return vca_dyn_smem + (a - (uint32_t)__cvta_generic_to_shared(vca_dyn_smem));
+    return (uint32_t)(reinterpret_cast<const uint8_t *>(p) - vca_dyn_smem);
 }
-__device__ __forceinline__ uint32_t lds32(uint32_t a) { return *reinterpret_cast<const uint32_t *>(smem_ptr(a)); }
-__device__ __forceinline__ uint2 lds64(uint32_t a) { return *reinterpret_cast<const uint2 *>(smem_ptr(a)); }
-#else
-__device__ __forceinline__ uint32_t lds32(uint32_t a)
+template <class T>
+__device__ __forceinline__ T lds(uint32_t off)
 {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
+    return *reinterpret_cast<const T *>(vca_dyn_smem + off);
 }
-__device__ __forceinline__ uint2 lds64(uint32_t a)
+template <class T>
+__device__ __forceinline__ void sts(uint32_t off, T v)
 {
-    uint2 v;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-    return v;
+    *reinterpret_cast<T *>(vca_dyn_smem + off) = v;
 }
-#endif
-__device__ __forceinline__ double lds_f64(uint32_t a)
-{
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts_f64(uint32_t a, double v)
-{
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
-}
-__device__ __forceinline__ void sts_v3u32(uint32_t a, uint32_t x, uint32_t y, uint32_t z)
-{
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(0u) : "memory");
-}
-__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
-{
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-#ifndef VCA_ASMLOADS
-__device__ __forceinline__ uint4 lds128(uint32_t a) { return *reinterpret_cast<const uint4 *>(smem_ptr(a)); }
-#else
-__device__ __forceinline__ uint4 lds128(uint32_t a)
-{
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-    return v;
-}
-#endif
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) { return lds<uint8_t>(a); }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) { return lds<uint16_t>(a); }
+__device__ __forceinline__ uint32_t lds32(uint32_t a) { return lds<uint32_t>(a); }
+__device__ __forceinline__ uint2 lds64(uint32_t a) { return lds<uint2>(a); }
+__device__ __forceinline__ uint4 lds128(uint32_t a) { return lds<uint4>(a); }
+__device__ __forceinline__ double lds_f64(uint32_t a) { return lds<double>(a); }
 
 // One sample of a unit in a swizzled box (row, column within the unit), 10-bit clamp
 template <int ES, int IB>
@@ -903,12 +865,22 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 //    warpgroup 0 = producers (warp g < G feeds group g; setmaxnreg.dec to VCA_PREG),
 //    warpgroups 1..G = consumer groups of 4 warps (setmaxnreg.inc to VCA_CREG), each group
 //    with its own ring, walking its own item sequence exactly like one legacy CTA.
-#ifndef VCA_PREG
-#define VCA_PREG 40  // producer warpgroup (24 spills the producer loop)
+// Register split (G = 3): producers dec to PREG, consumers inc to CREG <= 128 + (128 - PREG)
+// * 128 / 384.  A/B: 24/160 for the n = 16 luma families (config 3 +1..3 %, config 4 +4 %;
+// the producer loop spills a few bytes), 40/152 for n = 32 (config 2: 160 is -4 %).
+template <class F>
+struct Regs {
+#ifdef VCA_PREG
+    static constexpr int P = VCA_PREG;
+#else
+    static constexpr int P = VCA_GROUPS == 3 && F::NY == 16 ? 24 : 40;
 #endif
-#ifndef VCA_CREG
-#define VCA_CREG (VCA_GROUPS == 2 ? 232 : VCA_GROUPS == 3 ? 152 : 104)  // 65536 / threads + released
+#ifdef VCA_CREG
+    static constexpr int C = VCA_CREG;
+#else
+    static constexpr int C = VCA_GROUPS == 2 ? 232 : VCA_GROUPS == 3 ? (F::NY == 16 ? 160 : 152) : 104;
 #endif
+};
 constexpr int kGroups = VCA_GROUPS;
 constexpr int kGv = kGroups ? kGroups : 1;  // consumer groups per CTA
 constexpr int kFusedThreads = kGroups ? 128 * (1 + kGroups) : 160;
@@ -931,11 +903,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
 {
     using F = Fam<W_, BD_, LP_>;
     constexpr int NY = F::NY, NC = F::NC, W = F::W, WC = F::WC, NU = F::NU;
-#ifndef VCA_ASMLOADS
     uint8_t *smem_raw = vca_dyn_smem;
-#else
-    extern __shared__ uint8_t smem_raw[];
-#endif
     using Y = Lay<F>;
     uint8_t *smem0p = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     double *wtab = reinterpret_cast<double *>(smem0p + Y::WTAB_OFF);
@@ -979,7 +947,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
     if (kGroups ? warp < 4 : warp == 0) {
         // ---------------- TMA producer (A1)
 #if VCA_GROUPS
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(VCA_PREG));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Regs<F>::P));
 #endif
         if (lane == 0 && warp < kGv) {
             uint64_t policy;
@@ -1019,11 +987,11 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
 
     // ---------------- consumers
 #if VCA_GROUPS
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(VCA_CREG));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Regs<F>::C));
 #endif
     const int u = kGroups ? (warp & 3) : warp - 1;
     const int g = lane >> 2, t = lane & 3;
-    const uint32_t hst = smem_u32(stash) + (grp * 4 + u) * F::STASH;  // [32][9] doubles
+    const uint32_t hst = smem_off(stash) + (grp * 4 + u) * F::STASH;  // [32][9] doubles
     const uint32_t sxs = hst + 32 * 9 * 8;                 // [32][4] uint32
     UnitCtx<F> U;
     build_lane_const(U.L, a.T_all, g, t, NY);
@@ -1041,15 +1009,15 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
         for (int e = 0; e < UnitCtx<F>::NWC; ++e)
             U.wc[e] = NC == 16 ? U.wl16[e] : __ldg(W8 + g * 8 + 2 * t + e);
     }
-    U.wtab = smem_u32(wtab) + lane * 8;
+    U.wtab = smem_off(wtab) + lane * 8;
     {
         // [e][lane] weight table (same values as the registers; filled by consumer warp 0)
-        const uint32_t wsm0 = smem_u32(smem0p + Y::WSM_OFF) + grp * 10 * 32 * 8;
+        const uint32_t wsm0 = smem_off(smem0p + Y::WSM_OFF) + grp * 10 * 32 * 8;
         if (u == 0) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) sts_f64(wsm0 + (e * 32 + lane) * 8, U.wl16[e]);
+            for (int e = 0; e < 8; ++e) sts<double>(wsm0 + (e * 32 + lane) * 8, U.wl16[e]);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) sts_f64(wsm0 + ((8 + e) * 32 + lane) * 8, NC == 8 ? U.wc[e] : 0.0);
+            for (int e = 0; e < 2; ++e) sts<double>(wsm0 + ((8 + e) * 32 + lane) * 8, NC == 8 ? U.wc[e] : 0.0);
         }
         U.wsm = wsm0 + lane * 8;
         asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");  // this group's consumer warps
@@ -1057,7 +1025,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
     U.g = g;
     U.t = t;
     const double invNY = 1.0 / NY, invNC = 1.0 / NC;
-    const uint32_t smem0 = smem_u32(smem);
+    const uint32_t smem0 = smem_off(smem);  // stage boxes: data offsets
     const uint32_t full0 = smem_u32(full);
     const int64_t CY = (int64_t)rows * cols;
 
@@ -1096,7 +1064,6 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
             const int c0 = s * F::UNITS + u;
 #ifndef VCA_NULL_COMPUTE
             UnitOut o[NU];
-            bool valid[NU];
             if (s < s_fast) {
                 uint32_t bY[NU], bU[NU];
                 int64_t kk[NU];
@@ -1105,16 +1072,22 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     bY[n] = base + offY[n];
                     bU[n] = base + offU[n];
                     kk[n] = DUMP ? (int64_t)r * cols + c0 + 4 * n : 0;
-                    valid[n] = true;
                 }
                 process_units<F, false, DUMP, NU>(U, a, bY, bU, ubYc, ubCc, hvY, hvC, W, WC, kk, o, hu, hv, ca);
+                // stash: per-unit luma row-group partials and raw C_00 values, reduced 32 units
+                // at a time (NU divides 32, so the strip's slots are consecutive)
+                const uint32_t sl0 = (uint32_t)(s * NU) & 31u;
+#pragma unroll
+                for (int n = 0; n < NU; ++n) {
+                    if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, o[n].hY);
+                    if (lane == 0) sts<uint4>(sxs + (sl0 + n) * 16, make_uint4(o[n].dcY, o[n].dcU, o[n].dcV, 0u));
+                }
             } else {
                 // ragged strip end or a partial last block column: one unit at a time
 #pragma unroll
                 for (int n = 0; n < NU; ++n) {
                     const int c = c0 + 4 * n;
-                    valid[n] = c < cols;
-                    if (!valid[n]) continue;
+                    if (c >= cols) continue;
                     const int v = u + 4 * n;
                     const uint32_t bY[1] = {base + (v / F::UPB_Y) * F::BOXB_Y};
                     const uint32_t bU[1] = {base + F::ST_Y + (v / F::UPB_C) * F::BOXB_C};
@@ -1126,18 +1099,10 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                         process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1, hu, hv, ca);
                     else
                         process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1, hu, hv, ca);
-                    o[n] = o1[0];
+                    const uint32_t slot = (uint32_t)(s * NU + n) & 31u;
+                    if (t == 0) sts<double>(hst + (slot * 9 + g) * 8, o1[0].hY);
+                    if (lane == 0) sts<uint4>(sxs + slot * 16, make_uint4(o1[0].dcY, o1[0].dcU, o1[0].dcV, 0u));
                 }
-            }
-#pragma unroll
-            for (int n = 0; n < NU; ++n) {
-                if (!valid[n]) continue;
-                const int slot = (s * NU + n) & 31;
-                // stash: per-unit luma row-group partials and DC sums, reduced 32 units at a time
-                if (t == 0) sts_f64(hst + (slot * 9 + g) * 8, o[n].hY);
-                if (lane == 0)  // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
-                    sts_v3u32(sxs + slot * 16, (uint32_t)o[n].dcY >> 12, (uint32_t)o[n].dcU >> 12,
-                              (uint32_t)o[n].dcV >> 12);
             }
 #endif
             __syncwarp();
@@ -1166,9 +1131,11 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                 if (lane <= (mlast & 31) && cl < cols) {
 #pragma unroll
                     for (int gg = 0; gg < 8; ++gg) Hl += lds_f64(hst + (lane * 9 + gg) * 8);
-                    LYl = sqrt((double)lds32(sxs + lane * 16 + 0) * invNY);
-                    LUl = sqrt((double)lds32(sxs + lane * 16 + 4) * invNC);
-                    LVl = sqrt((double)lds32(sxs + lane * 16 + 8) * invNC);
+                    // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
+                    const uint4 dc = lds<uint4>(sxs + lane * 16);
+                    LYl = sqrt((double)(dc.x >> 12) * invNY);
+                    LUl = sqrt((double)(dc.y >> 12) * invNC);
+                    LVl = sqrt((double)(dc.z >> 12) * invNC);
                     HYrow[cl] = Hl;
                 }
 #pragma unroll
