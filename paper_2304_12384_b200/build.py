@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2,-Wall",
+    "-Xcompiler", "-fPIC,-O2,-Wall,-pthread",
     "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
     "-shared", "-cudart", "static",
@@ -28,7 +28,7 @@ NVCC_FLAGS = [
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
-                  + [os.path.join(ROOT, "include", "vca.h")])
+                  + glob.glob(os.path.join(CSRC, "*.cpp")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def stale() -> bool:
@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         return LIB
     tmp = target + ".tmp%d" % os.getpid()
     cmd = [NVCC] + NVCC_FLAGS + ["-D" + d for d in defines] + ["-I", os.path.join(ROOT, "include"), "-o", tmp,
-                                                                 os.path.join(CSRC, "vca_api.cu")]
+                                                                 os.path.join(CSRC, "vca_api.cu"),
+                                                                 os.path.join(CSRC, "vca_io.cpp")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as fh:

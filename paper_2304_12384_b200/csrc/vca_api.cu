@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/vca.h"
+#include "../../include/vca_io.h"
 #include "kernel_finalize.cuh"
 #include "kernel_fused.cuh"
 #include "kernel_generic.cuh"
@@ -247,6 +248,13 @@ const char *vca_status_string(int status)
     case VCA_ERR_CUDA: return "CUDA error (context poisoned)";
     case VCA_ERR_OOM: return "out of device memory";
     case VCA_ERR_SCRATCH: return "scratch buffer too small";
+    case VCA_IO_EOF: return "end of stream";
+    case VCA_ERR_IO: return "I/O error (open, read or write)";
+    case VCA_ERR_MALFORMED_MAGIC: return "not a Y4M stream (missing YUV4MPEG2 magic)";
+    case VCA_ERR_MALFORMED_HEADER: return "malformed Y4M header or stream geometry";
+    case VCA_ERR_TRUNCATED_FRAME: return "truncated frame";
+    case VCA_ERR_MALFORMED_FRAME_MARKER: return "malformed Y4M FRAME marker";
+    case VCA_ERR_INTERLACED: return "interlaced Y4M stream (progressive only)";
     default: return "unknown status";
     }
 }

@@ -18,6 +18,8 @@ STATUS = {
     0: "VCA_OK", -1: "VCA_ERR_INVALID_ARG", -2: "VCA_ERR_UNSUPPORTED_BLOCK_SIZE",
     -3: "VCA_ERR_UNSUPPORTED_BIT_DEPTH", -4: "VCA_ERR_UNSUPPORTED_CHROMA", -5: "VCA_ERR_GEOMETRY",
     -6: "VCA_ERR_ALIGNMENT", -7: "VCA_ERR_CUDA", -8: "VCA_ERR_OOM", -9: "VCA_ERR_SCRATCH",
+    1: "VCA_IO_EOF", -10: "VCA_ERR_IO", -11: "VCA_ERR_MALFORMED_MAGIC", -12: "VCA_ERR_MALFORMED_HEADER",
+    -13: "VCA_ERR_TRUNCATED_FRAME", -14: "VCA_ERR_MALFORMED_FRAME_MARKER", -15: "VCA_ERR_INTERLACED",
 }
 PATHS = {1: "fused_mma", 2: "warp_generic"}
 CHROMA = {420: 0, 422: 1, 444: 2}
@@ -28,10 +30,12 @@ RECORD_DTYPE = np.dtype(
 )
 FEATURES = ("E_Y", "h", "L_Y", "E_U", "L_U", "E_V", "L_V")
 
-# every symbol include/vca.h declares
+# every symbol include/vca.h and include/vca_io.h declare
 EXPORTS = ("vca_create", "vca_get_info", "vca_scratch_bytes", "vca_analyze", "vca_analyze_host", "vca_reset",
            "vca_profile_enable", "vca_profile_read", "vca_debug_dump", "vca_destroy", "vca_status_string",
-           "vca_version")
+           "vca_version",
+           "vca_y4m_parse_header", "vca_y4m_open", "vca_raw_open", "vca_reader_read", "vca_reader_frames",
+           "vca_reader_warnings", "vca_reader_close", "vca_analyze_stream", "vca_write_csv", "vca_summarize")
 
 
 class VcaError(RuntimeError):
@@ -80,6 +84,21 @@ def lib():
     L.vca_status_string.argtypes = [c_int]
     L.vca_status_string.restype = ctypes.c_char_p
     L.vca_version.restype = ctypes.c_char_p
+    # include/vca_io.h
+    cp, sz = ctypes.c_char_p, ctypes.c_size_t
+    L.vca_y4m_parse_header.argtypes = [cp, sz, vp, ctypes.POINTER(sz), ctypes.POINTER(c_int)]
+    L.vca_y4m_open.argtypes = [cp, ctypes.POINTER(vp), vp]
+    L.vca_raw_open.argtypes = [cp, c_int, c_int, c_int, c_int, ctypes.POINTER(vp), vp]
+    L.vca_reader_read.argtypes = [vp, c_int, P3, I3, I3, ctypes.POINTER(c_int)]
+    L.vca_reader_frames.argtypes = [vp]
+    L.vca_reader_frames.restype = i64
+    L.vca_reader_warnings.argtypes = [vp]
+    L.vca_reader_close.argtypes = [vp]
+    L.vca_reader_close.restype = None
+    L.vca_analyze_stream.argtypes = [vp, vp, c_int, vp, i64, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double)]
+    L.vca_write_csv.argtypes = [cp, vp, i64]
+    L.vca_write_csv.restype = i64
+    L.vca_summarize.argtypes = [vp, i64, vp, vp]
     _lib = L
     return L
 

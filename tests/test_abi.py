@@ -1,5 +1,5 @@
 """C-ABI boundary checks that need no GPU: libvca.so builds for sm_100a,
-loads, exports every symbol include/vca.h declares, and validates arguments
+loads, exports every symbol include/vca.h and include/vca_io.h declare, and validates arguments
 before touching CUDA."""
 import ctypes
 import os
@@ -14,9 +14,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_functions():
-    src = open(os.path.join(ROOT, "include", "vca.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("vca.h", "vca_io.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(vca_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(vca_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_and_binding_agree():
@@ -26,7 +26,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_declared_symbol():
     L = vca.lib()
     out = subprocess.run(["nm", "-D", "--defined-only", vca._build.LIB], capture_output=True, text=True).stdout
-    exported = set(re.findall(r"\bT (vca_[a-z_]+)\b", out))
+    exported = set(re.findall(r"\bT (vca_[a-z0-9_]+)\b", out))
     for name in declared_functions():
         assert hasattr(L, name)
         assert name in exported, name
