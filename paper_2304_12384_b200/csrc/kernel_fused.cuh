@@ -59,9 +59,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
 // Blocking wait on an mbarrier phase; the suspend-time hint lets the warp sleep
@@ -187,9 +187,12 @@ struct Fam {
 #ifndef VCA_NU
 #define VCA_NU (VCA_GROUPS == 3 ? 4 : 2)
 #endif
+#ifndef VCA_NU32
+#define VCA_NU32 2  // units per consumer warp per strip for the n = 32 luma path (A/B: 1 -> 2 +3 %)
+#endif
     // units per consumer warp per strip (ILP, per-strip overhead); 4 only while a 16-unit stage
     // stays <= 24 KB (two stages per group, three groups per CTA)
-    static constexpr int NU = (NY != 16) ? 1 : (VCA_NU == 4 && 24 * ES * W * W > 24576) ? 2 : VCA_NU;
+    static constexpr int NU = (NY != 16) ? VCA_NU32 : (VCA_NU == 4 && 24 * ES * W * W > 24576) ? 2 : VCA_NU;
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
     static constexpr int IB_Y = (UNITS * RB_Y) < 128 ? UNITS * RB_Y : 128;  // box inner bytes = swizzle span
@@ -525,7 +528,7 @@ struct UnitCtx {
     LaneConst L;
     double wl16[8];     // luma n = 16 weights at this lane's 8 positions
     double wc[NWC];     // chroma weights at this lane's positions
-    uint32_t wtab;      // smem address of this lane's luma n = 32 weights ([slot][lane] doubles)
+    uint32_t wtab;      // smem offset of this lane's luma n = 32 weights ([pair][lane] double2)
     uint32_t wsm;       // smem address of this lane's n = 16 / 8 weights ([e][lane])
     int g, t;
 };
@@ -670,51 +673,67 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             }
         }
     } else {
-        static_assert(NY != 32 || NU == 1, "n = 32 luma runs one unit per warp");
-        // n = 32: pass 1 over 4 n-tiles (y = 8q + g), 2 m-tiles (j = 16mt + g (+8))
-        int32_t D1[2][4][4];
+        // n = 32: pass 1 over 4 n-tiles (y = 8q + g), 2 m-tiles (j = 16mt + g (+8)); NU units
+        // as independent instruction streams
+        int32_t D1[NU][2][4][4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t l0, h0, l1, h1;
-            load4<F, 0>(boxY[0], ubY[0], 8 * q + g, t, hvY, wvY, XPART, l0, h0);
-            load4<F, 0>(boxY[0], ubY[0], 8 * q + g, 4 + t, hvY, wvY, XPART, l1, h1);
+        for (int n = 0; n < NU; ++n)
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                mma32_su(D1[mt][q], L.t32[mt], l0, l1);
-                if (ES == 2) {
-                    int32_t Dh[4];
-                    mma32_su(Dh, L.t32[mt], h0, h1);
+            for (int q = 0; q < 4; ++q) {
+                uint32_t l0, h0, l1, h1;
+                load4<F, 0>(boxY[n], ubY[n], 8 * q + g, t, hvY, wvY, XPART, l0, h0);
+                load4<F, 0>(boxY[n], ubY[n], 8 * q + g, 4 + t, hvY, wvY, XPART, l1, h1);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) D1[mt][q][e] = (int32_t)((uint32_t)D1[mt][q][e] + ((uint32_t)Dh[e] << 8));
+                for (int mt = 0; mt < 2; ++mt) {
+                    mma32_su(D1[n][mt][q], L.t32[mt], l0, l1);
+                    if (ES == 2) {
+                        int32_t Dh[4];
+                        mma32_su(Dh, L.t32[mt], h0, h1);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            D1[n][mt][q][e] = (int32_t)((uint32_t)D1[n][mt][q][e] + ((uint32_t)Dh[e] << 8));
+                    }
                 }
             }
-        }
-        double hacc = 0.0;
+        // four independent FMA chains per unit (one per fragment slot e), combined in a fixed order
+        double hacc[NU][4];
+#pragma unroll
+        for (int n = 0; n < NU; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hacc[n][e] = 0.0;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
             const int ms = rr >> 1, hf = rr & 1;
-            uint32_t b0a, b1a, b2a, b0b, b1b, b2b;
-            byte_planes(D1[ms][0][2 * hf], D1[ms][0][2 * hf + 1], D1[ms][1][2 * hf], D1[ms][1][2 * hf + 1], b0a, b1a,
-                        b2a);
-            byte_planes(D1[ms][2][2 * hf], D1[ms][2][2 * hf + 1], D1[ms][3][2 * hf], D1[ms][3][2 * hf + 1], b0b, b1b,
-                        b2b);
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                int32_t E0[4], E1[4], E2[4];
-                mma32_su(E0, L.p32[mt], b0a, b0b);
-                mma32_su(E1, L.p32[mt], b1a, b1b);
-                mma32_ss(E2, L.p32[mt], b2a, b2b);
+            for (int n = 0; n < NU; ++n) {
+                uint32_t b0a, b1a, b2a, b0b, b1b, b2b;
+                byte_planes(D1[n][ms][0][2 * hf], D1[n][ms][0][2 * hf + 1], D1[n][ms][1][2 * hf],
+                            D1[n][ms][1][2 * hf + 1], b0a, b1a, b2a);
+                byte_planes(D1[n][ms][2][2 * hf], D1[n][ms][2][2 * hf + 1], D1[n][ms][3][2 * hf],
+                            D1[n][ms][3][2 * hf + 1], b0b, b1b, b2b);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int32_t cc = combine3(E0[e], E1[e], E2[e]);
-                    hacc = fma(lds_f64(U.wtab + ((mt * 4 + rr) * 4 + e) * 32 * 8), fabs(i2d(cc)), hacc);
-                    if (mt == 0 && rr == 0 && e == 0) o[0].dcY = cc;
-                    if (DUMP)
-                        a.dump.coeffs[0][k[0] * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] = cc;
+                for (int mt = 0; mt < 2; ++mt) {
+                    int32_t E0[4], E1[4], E2[4];
+                    mma32_su(E0, L.p32[mt], b0a, b0b);
+                    mma32_su(E1, L.p32[mt], b1a, b1b);
+                    mma32_ss(E2, L.p32[mt], b2a, b2b);
+                    const double2 w01 = lds<double2>(U.wtab + ((mt * 4 + rr) * 2 + 0) * 512);
+                    const double2 w23 = lds<double2>(U.wtab + ((mt * 4 + rr) * 2 + 1) * 512);
+                    const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int32_t cc = combine3(E0[e], E1[e], E2[e]);
+                        hacc[n][e] = fma(wv[e], fabs(i2d(cc)), hacc[n][e]);
+                        if (mt == 0 && rr == 0 && e == 0) o[n].dcY = cc;
+                        if (DUMP)
+                            a.dump.coeffs[0][k[n] * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] =
+                                cc;
+                    }
                 }
             }
         }
-        hY[0] = hacc;
+#pragma unroll
+        for (int n = 0; n < NU; ++n) hY[n] = (hacc[n][0] + hacc[n][1]) + (hacc[n][2] + hacc[n][3]);
     }
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
@@ -784,50 +803,53 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             }
         }
     } else {
-        static_assert(NC != 16 || NU == 1, "n = 16 chroma pairs with n = 32 luma");
 #pragma unroll
-        for (int pl = 1; pl <= 2; ++pl) {
-            const uint32_t box = pl == 1 ? boxU[0] : boxU[0] + F::ST_C;
-            uint32_t blo[2], bhi[2];
+        for (int n = 0; n < NU; ++n)
 #pragma unroll
-            for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC[0], 8 * q + g, t, hvC, wvC, XPART, blo[q], bhi[q]);
-            int32_t C[2][4];
-            dct16<ES>(L, blo, bhi, C);
-            double hacc = 0.0;
-            if (ChromaAcc<F>::ON) {
+            for (int pl = 1; pl <= 2; ++pl) {
+                const uint32_t box = pl == 1 ? boxU[n] : boxU[n] + F::ST_C;
+                uint32_t blo[2], bhi[2];
 #pragma unroll
-                for (int p = 0; p < 2; ++p)
+                for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC[n], 8 * q + g, t, hvC, wvC, XPART, blo[q], bhi[q]);
+                int32_t C[2][4];
+                dct16<ES>(L, blo, bhi, C);
+                double hacc = 0.0;
+                if (ChromaAcc<F>::ON) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if (pl == 1)
-                            ca.u[p * 4 + e] += (uint32_t)abs(C[p][e]);
-                        else
-                            ca.v[p * 4 + e] += (uint32_t)abs(C[p][e]);
-                    }
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            if (pl == 1)
+                                ca.u[p * 4 + e] += (uint32_t)abs(C[p][e]);
+                            else
+                                ca.v[p * 4 + e] += (uint32_t)abs(C[p][e]);
+                        }
+                }
+                if (!ChromaAcc<F>::ON || DUMP) {
+                    double h2[2] = {0.0, 0.0};  // two chains, fixed combination
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) h2[p] = fma(U.wc[p * 4 + e], fabs(i2d(C[p][e])), h2[p]);
+                    hacc = h2[0] + h2[1];
+                }
+                if (pl == 1) {
+                    o[n].hu = hacc;
+                    o[n].dcU = C[0][0];
+                    if (!ChromaAcc<F>::ON) hu_acc += hacc;
+                } else {
+                    o[n].hv = hacc;
+                    o[n].dcV = C[0][0];
+                    if (!ChromaAcc<F>::ON) hv_acc += hacc;
+                }
+                if (DUMP) {
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            a.dump.coeffs[pl][k[n] * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
+                }
             }
-            if (!ChromaAcc<F>::ON || DUMP) {
-#pragma unroll
-                for (int p = 0; p < 2; ++p)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) hacc = fma(U.wc[p * 4 + e], fabs(i2d(C[p][e])), hacc);
-            }
-            if (pl == 1) {
-                o[0].hu = hacc;
-                o[0].dcU = C[0][0];
-                if (!ChromaAcc<F>::ON) hu_acc += hacc;
-            } else {
-                o[0].hv = hacc;
-                o[0].dcV = C[0][0];
-                if (!ChromaAcc<F>::ON) hv_acc += hacc;
-            }
-            if (DUMP) {
-#pragma unroll
-                for (int p = 0; p < 2; ++p)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        a.dump.coeffs[pl][k[0] * 256 + (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1)] = C[p][e];
-            }
-        }
     }
     if (DUMP) {
 #pragma unroll
@@ -928,11 +950,13 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (F::WTAB) {
-        // luma n = 32 weights in [slot][lane] order: slot = (mt*4 + r)*4 + e, lane (g, t):
-        // i = 16mt + g + 8(e>>1), j = 8r + 2t + (e&1)
+        // luma n = 32 weights in [slot pair][lane][2] order (one conflict-free LDS.128 per pair):
+        // slot = (mt*4 + r)*4 + e = 2 * pair + (e & 1), lane (g, t): i = 16mt + g + 8(e>>1),
+        // j = 8r + 2t + (e&1)
         const double *W32 = a.W_all + table_offset(32);
         for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
-            const int slot = idx >> 5, ln = idx & 31, gg = ln >> 2, tt = ln & 3;
+            const int ln = (idx >> 1) & 31, gg = ln >> 2, tt = ln & 3;
+            const int slot = 2 * (idx >> 6) + (idx & 1);
             const int e = slot & 3, r = (slot >> 2) & 3, mt = slot >> 4;
             const int i = 16 * mt + gg + 8 * (e >> 1), j = 8 * r + 2 * tt + (e & 1);
             wtab[idx] = W32[i * 32 + j];
@@ -1009,7 +1033,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
         for (int e = 0; e < UnitCtx<F>::NWC; ++e)
             U.wc[e] = NC == 16 ? U.wl16[e] : __ldg(W8 + g * 8 + 2 * t + e);
     }
-    U.wtab = smem_off(wtab) + lane * 8;
+    U.wtab = smem_off(wtab) + lane * 16;
     {
         // [e][lane] weight table (same values as the registers; filled by consumer warp 0)
         const uint32_t wsm0 = smem_off(smem0p + Y::WSM_OFF) + grp * 10 * 32 * 8;
@@ -1026,7 +1050,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
     U.t = t;
     const double invNY = 1.0 / NY, invNC = 1.0 / NC;
     const uint32_t smem0 = smem_off(smem);  // stage boxes: data offsets
-    const uint32_t full0 = smem_u32(full);
+    const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
     const int64_t CY = (int64_t)rows * cols;
 
     // per-warp constants: smem offsets of this warp's units inside a stage, and the number of
@@ -1106,7 +1130,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
             }
 #endif
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
             if (++st == F::STAGES) {
                 st = 0;
                 phase ^= 1;
