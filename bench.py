@@ -138,10 +138,15 @@ def cpu_oracle_fps(Y, U, V, bd, block, lowpass, target_s=10.0, max_frames=None):
     n = max(1, min(F, int(target_s * cores / max(one, 1e-3))))
     if max_frames:
         n = min(n, max_frames)
-    t0 = time.perf_counter()
-    oracle.analyze(npl[0][:n], npl[1][:n], npl[2][:n], bd, block, lowpass, n_threads=cores)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt, cores
+    # repeat passes over the sample until about target_s of CPU work has been timed
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.analyze(npl[0][:n], npl[1][:n], npl[2][:n], bd, block, lowpass, n_threads=cores)
+        done += n
+        dt = time.perf_counter() - t0
+        if dt >= target_s:
+            break
+    return done / dt, done, dt, cores
 
 
 def run_reference(args, rank, world):
@@ -334,6 +339,8 @@ def main():
         fr = (world if world > 1 else 1) * (ne - n_halo)
         line["e2e"] = {"value": fr * e_steps / dt, "unit": "frames/s", "h2d_bytes_per_step": ne * fb,
                        "d2h_bytes_per_step": (ne - n_halo) * 64, "frames_per_step": ne,
+                       "h2d_gbs": ne * fb * e_steps / dt / 1e9 / (world if world > 1 else 1),
+                       "bound": "PCIe host-to-device copy of the frames (the kernels take < 1 % of the time)",
                        "api": "vca_analyze_host (pinned host memory, 8-frame chunks, copy/compute overlap)"}
         del hY, hU, hV, ae
 
@@ -342,7 +349,8 @@ def main():
         ns = min(nfr, 160)
         fps, n, dt, cores = cpu_oracle_fps(Y[:ns].cpu(), U[:ns].cpu(), V[:ns].cpu(), bd, c.block_size, c.lowpass)
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
-                                "sample": "%d frames of the same workload, %.1f s, OpenMP over frames" % (n, dt)}
+                                "sample": "%d frame analyses (repeated passes over the first %d frames of the same "
+                                          "workload), %.1f s, OpenMP over frames" % (n, ns, dt)}
     if rank == 0:
         # parity spot check of the timed output (first and last record) is done in tests; here sanity only
         rec = records_to_numpy(gathered[0] if world > 1 else out)
