@@ -81,7 +81,19 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("name,W,H,bd,w,lp", CASES, ids=[c[0] for c in CASES])
+# Several whole strips of the fused kernel (16 units per strip for n = 16 luma, 8 for
+# n = 32 and for the 10-bit low-pass family) plus a ragged strip end, a partial last block
+# column inside a strip and a partial last block row.
+CASES_STRIPS = [
+    ("strips_lp32", 1174, 100, 8, 32, True),          # 37 cols: 2 x 16 + 5, last col 22/32 wide
+    ("strips_full16_10bit", 586, 72, 10, 16, False),   # 37 cols, last col 10/16 wide
+    ("strips_full32", 602, 76, 8, 32, False),          # 19 cols: 2 x 8 + 3, last col 26/32 wide
+    ("strips_lp32_10bit", 602, 68, 10, 32, True),      # 19 cols (8-unit strips)
+    ("strips_full16_8bit", 1040, 40, 8, 16, False),    # 65 cols: 4 x 16 + 1
+]
+
+
+@pytest.mark.parametrize("name,W,H,bd,w,lp", CASES + CASES_STRIPS, ids=[c[0] for c in CASES + CASES_STRIPS])
 def test_parity_small(name, W, H, bd, w, lp):
     F = 4
     Y, U, V = synth.g_frames(17, W, H, F, bd)
@@ -211,3 +223,13 @@ def test_parity_full_size_sampled(cfg):
         assert_records(g[t:t + 1], r)
     Yc, Uc, Vc = (p[F - 1:F].cpu() for p in (Y, U, V))
     check_dump(a, Yc, Uc, Vc, c.bit_depth, c.block_size, c.lowpass, frame=0)
+
+
+@pytest.mark.slow
+def test_parity_8k_two_frames():
+    """Largest geometry in use (8K UHD-2, 7680x4320, block 32 low-pass and full): all seven
+    features of both frames (h across them) against the oracle."""
+    Y, U, V = synth.g_frames(21, 7680, 4320, 2, 8)
+    for lp in (True, False):
+        g, r, a = run_both(Y, U, V, 8, 32, lp)
+        assert_records(g, r)
