@@ -29,6 +29,7 @@
 //    partial sums in a fixed order (A7 inputs, R-11).
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "kernel_generic.cuh"
 #include "vca_common.cuh"
@@ -134,6 +135,24 @@ __device__ __forceinline__ void mma32_uu_acc(int32_t (&d)[4], const uint32_t (&a
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]));
 }
 
+// D = A(f16) . B(f16) + C (f32), m16n8k16 -- the exact 10-bit pass 1 (see dct16h)
+__device__ __forceinline__ void mma16_h(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1, float c)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%10,%10,%10};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c));
+}
+// pass 2 with a per-lane accumulator init (the corrections of the 10-bit path)
+__device__ __forceinline__ void mma16_su_c(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b, int32_t c0,
+                                           int32_t c1, int32_t c2, int32_t c3)
+{
+    VCA_MMA_ASM("mma.sync.aligned.m16n8k16.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+                 : "r"(a0), "r"(a1), "r"(b), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
+
 // byte planes b = 0, 1, 2 of four int32 values (v0..v3 -> bytes 0..3 of each plane)
 __device__ __forceinline__ void byte_planes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t &p0,
                                             uint32_t &p1, uint32_t &p2)
@@ -209,6 +228,13 @@ struct Fam {
     static constexpr int RING = VCA_RING;  // ring bytes per CTA (several CTAs per SM)
     static constexpr int STAGES = (RING / STAGE) < 2 ? 2 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);
+#ifndef VCA_NO_HMMA10
+    // 10-bit n = 16 / paired n = 8 pass 1 on f16 tensor cores (one HMMA instead of a lo/hi
+    // pair of IMMAs plus their recombination; exact, see dct16h)
+    static constexpr bool H10 = (ES == 2) && (NY == 16);
+#else
+    static constexpr bool H10 = false;
+#endif
 #ifndef VCA_MINB
 #define VCA_MINB 3
 #endif
@@ -303,7 +329,10 @@ __device__ __forceinline__ uint32_t pair_sum16(uint32_t v)
 // Four consecutive DCT-input samples x = 4xg..4xg+3 of row y of one unit, as
 // byte planes lo (and hi for 10-bit).  hv/wv: valid rows/columns of the unit in
 // source samples (edge replication by clamping); xpart: wv < block width.
-template <class F, int PL>
+// HALF (10-bit H10 path): lo = f16x2 {x0, x1}, hi = f16x2 {x2, x3}, each sample v <= 1023
+// as the f16 bit pattern 0x6400 | v, i.e. the value 1024 + v (exact; the 1024 offset is
+// removed in dct16h / dct8pairh).
+template <class F, int PL, bool HALF = false>
 __device__ __forceinline__ void load4(uint32_t box, int ub, int y, int xg, int hv, int wv, bool xpart,
                                       uint32_t &lo, uint32_t &hi)
 {
@@ -321,8 +350,13 @@ __device__ __forceinline__ void load4(uint32_t box, int ub, int y, int xg, int h
                 uint2 v = lds64(box + swz<IB>(row * IB + ub0 + 8 * xg));
                 v.x = __vminu2(v.x, 0x03FF03FFu);
                 v.y = __vminu2(v.y, 0x03FF03FFu);
-                lo = __byte_perm(v.x, v.y, 0x6420);
-                hi = __byte_perm(v.x, v.y, 0x7531);
+                if (HALF) {
+                    lo = v.x | 0x64006400u;
+                    hi = v.y | 0x64006400u;
+                } else {
+                    lo = __byte_perm(v.x, v.y, 0x6420);
+                    hi = __byte_perm(v.x, v.y, 0x7531);
+                }
             }
         } else {
             const int r0 = min(2 * y, hv - 1), r1 = min(2 * y + 1, hv - 1);
@@ -340,8 +374,13 @@ __device__ __forceinline__ void load4(uint32_t box, int ub, int y, int xg, int h
                 const uint32_t d2 = (pair_sum16(__vminu2(a.z, C10)) + pair_sum16(__vminu2(b.z, C10)) + 2) >> 2;
                 const uint32_t d3 = (pair_sum16(__vminu2(a.w, C10)) + pair_sum16(__vminu2(b.w, C10)) + 2) >> 2;
                 const uint32_t p01 = d0 | (d1 << 16), p23 = d2 | (d3 << 16);
-                lo = __byte_perm(p01, p23, 0x6420);
-                hi = __byte_perm(p01, p23, 0x7531);
+                if (HALF) {
+                    lo = p01 | 0x64006400u;
+                    hi = p23 | 0x64006400u;
+                } else {
+                    lo = __byte_perm(p01, p23, 0x6420);
+                    hi = __byte_perm(p01, p23, 0x7531);
+                }
             }
         }
     } else {  // partial last block column: per-sample clamped reads
@@ -358,8 +397,15 @@ __device__ __forceinline__ void load4(uint32_t box, int ub, int y, int xg, int h
                 v = (box_sample<ES, IB>(box, ub0, r0, x0) + box_sample<ES, IB>(box, ub0, r0, x1) +
                      box_sample<ES, IB>(box, ub0, r1, x0) + box_sample<ES, IB>(box, ub0, r1, x1) + 2) >> 2;
             }
-            l |= (uint32_t)(v & 255) << (8 * k);
-            h |= (uint32_t)(v >> 8) << (8 * k);
+            if (HALF) {
+                if (k < 2)
+                    l |= (uint32_t)(v | 0x6400) << (16 * k);
+                else
+                    h |= (uint32_t)(v | 0x6400) << (16 * (k - 2));
+            } else {
+                l |= (uint32_t)(v & 255) << (8 * k);
+                h |= (uint32_t)(v >> 8) << (8 * k);
+            }
         }
         lo = l;
         hi = h;
@@ -377,6 +423,11 @@ struct LaneConst {
     // 2x2 low-pass as an MMA: B = 0/1 pair-sum matrix, k = 4t+i (+16) -> source column,
     // n = g -> output column; luma rl = [2t + (i>>1) == g], chroma rc = same over 16 columns
     uint32_t rl, rc;
+    // 10-bit f16 pass 1 (H10): A fragments (f16x2) of T16 and blockdiag(T8, T8) with the
+    // contraction slots permuted to the load4<HALF> sample order, and the lane-0 DC
+    // corrections of the pass-2 accumulators (dct16h, dct8pairh)
+    uint32_t h16[4], h8[4];
+    int32_t dcfix16, dcfix8e, dcfix8o;
 };
 
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d)
@@ -424,6 +475,37 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
             if (2 * t + (i >> 1) == g) r |= 1u << (8 * i);
         L.rl = r;
         L.rc = r;
+    }
+    if (NY == 16) {
+        // f16 A fragment (m16n8k16, row-major): reg 0 = A[g][2t, 2t+1], 1 = A[g+8][2t, 2t+1],
+        // 2 = A[g][2t+8, 2t+9], 3 = A[g+8][2t+8, 2t+9]; contraction slot (lane t, s) holds the
+        // sample load4<HALF> put there: s = 0, 1 -> x = 4t + s (reg lo), s = 2, 3 -> x = 4t + s (reg hi)
+        const int8_t *T16 = T_all + table_offset(16);
+        const int8_t *T8 = T_all + table_offset(8);
+        auto h2 = [](int a, int b) {
+            return (uint32_t)__half_as_ushort(__int2half_rn(a)) | ((uint32_t)__half_as_ushort(__int2half_rn(b)) << 16);
+        };
+        auto T16a = [&](int i, int x) { return (int)__ldg(T16 + i * 16 + x); };
+        auto T8a = [&](int i, int x) { return (int)__ldg(T8 + i * 8 + x); };
+        L.h16[0] = h2(T16a(g, 4 * t), T16a(g, 4 * t + 1));
+        L.h16[1] = h2(T16a(g + 8, 4 * t), T16a(g + 8, 4 * t + 1));
+        L.h16[2] = h2(T16a(g, 4 * t + 2), T16a(g, 4 * t + 3));
+        L.h16[3] = h2(T16a(g + 8, 4 * t + 2), T16a(g + 8, 4 * t + 3));
+        // chroma pair: lanes t < 2 load U columns 4(t&1).., lanes t >= 2 V; rows g: U freq g,
+        // rows g + 8: V freq g
+        const bool isU = t < 2;
+        const int xb = 4 * (t & 1);
+        L.h8[0] = isU ? h2(T8a(g, xb), T8a(g, xb + 1)) : 0u;
+        L.h8[1] = isU ? 0u : h2(T8a(g, xb), T8a(g, xb + 1));
+        L.h8[2] = isU ? h2(T8a(g, xb + 2), T8a(g, xb + 3)) : 0u;
+        L.h8[3] = isU ? 0u : h2(T8a(g, xb + 2), T8a(g, xb + 3));
+        // pass-2 accumulator corrections, mod 2^32 (dct16h / dct8pairh): the pixel offset 1024
+        // adds 1024 (64n)^2 to C_00 (2^30 for n = 16, 2^28 for n = 8); the plane-2 offset 64
+        // adds 2^16 * 64 * 64n to every C_0j (2^32 == 0 for n = 16, 2^31 for n = 8).  Lanes g = 0
+        // hold row i = 0; lane 0 slots e = 0 (and e = 2 for the V block) hold C_00.
+        L.dcfix16 = (g == 0 && t == 0) ? (int32_t)(0u - (1u << 30)) : 0;
+        L.dcfix8e = g == 0 ? (int32_t)((1u << 31) - (t == 0 ? (1u << 28) : 0u)) : 0;
+        L.dcfix8o = g == 0 ? (int32_t)(1u << 31) : 0;
     }
     if (NY == 32) {
         const int8_t *T32 = T_all + table_offset(32);
@@ -509,6 +591,58 @@ __device__ __forceinline__ void dct8pair(const LaneConst &L, uint32_t blo, uint3
 }
 
 
+
+// 10-bit n = 16 (H10): pass 1 on the f16 tensor cores.  B = 1024 + x (load4<HALF>), A = T16
+// (slot-permuted), C = 1.5 * 2^23: every product, partial sum and result is an integer of
+// magnitude < 2^24 around 1.5 * 2^23, so the f32 accumulation is exact and the result's bit
+// pattern is 0x4B400000 + Z' with Z' = Z + 2^20 [j = 0] (|Z'| < 2^22).  Its bytes 0, 1 are
+// Z' mod 2^16 and byte 2 is (Z' >> 16) + 64 (u8), so pass 2 runs on those three planes as
+// in dct16 (plane 2 unsigned) and the two offsets are removed mod 2^32 by the accumulator
+// init of the plane-0 MMA (LaneConst::dcfix16).  Output layout identical to dct16.
+__device__ __forceinline__ void dct16h(const LaneConst &L, const uint32_t (&blo)[2], const uint32_t (&bhi)[2],
+                                       int32_t (&C)[2][4])
+{
+    int32_t D1[2][4];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        float Df[4];
+        mma16_h(Df, L.h16, blo[q], bhi[q], 12582912.0f);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D1[q][e] = __float_as_int(Df[e]);
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        uint32_t b0, b1, b2;
+        byte_planes(D1[0][2 * p], D1[0][2 * p + 1], D1[1][2 * p], D1[1][2 * p + 1], b0, b1, b2);
+        int32_t E0[4], E1[4], E2[4];
+        if (p == 0)
+            mma16_su_c(E0, L.p16a0, L.p16a1, b0, L.dcfix16, 0, 0, 0);
+        else
+            mma16_su(E0, L.p16a0, L.p16a1, b0);
+        mma16_su(E1, L.p16a0, L.p16a1, b1);
+        mma16_su(E2, L.p16a0, L.p16a1, b2);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) C[p][e] = combine3(E0[e], E1[e], E2[e]);
+    }
+}
+
+// 10-bit paired n = 8 (H10): as dct16h with A = blockdiag(T8, T8) (slot-permuted); the
+// plane-2 offset adds 2^31 to every C_0j of both blocks and the pixel offset 2^28 to C_00
+// (LaneConst::dcfix8e / dcfix8o).  Output layout identical to dct8pair.
+__device__ __forceinline__ void dct8pairh(const LaneConst &L, uint32_t blo, uint32_t bhi, int32_t (&C)[4])
+{
+    float Df[4];
+    mma16_h(Df, L.h8, blo, bhi, 12582912.0f);
+    uint32_t b0, b1, b2;
+    byte_planes(__float_as_int(Df[0]), __float_as_int(Df[1]), __float_as_int(Df[2]), __float_as_int(Df[3]), b0, b1,
+                b2);
+    int32_t E0[4], E1[4], E2[4];
+    mma16_su_c(E0, L.p8a0, L.p8a1, b0, L.dcfix8e, L.dcfix8o, L.dcfix8e, L.dcfix8o);
+    mma16_su(E1, L.p8a0, L.p8a1, b1);
+    mma16_su(E2, L.p8a0, L.p8a1, b2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) C[e] = combine3(E0[e], E1[e], E2[e]);
+}
 
 // ------------------------------------------------------------------ kernel
 struct FusedArgs {
@@ -641,11 +775,16 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             for (int n = 0; n < NU; ++n)
 #pragma unroll
                 for (int q = 0; q < 2; ++q)
-                    load4<F, 0>(boxY[n], ubY[n], 8 * q + g, t, hvY, wvY, XPART, blo[n][q], bhi[n][q]);
+                    load4<F, 0, F::H10>(boxY[n], ubY[n], 8 * q + g, t, hvY, wvY, XPART, blo[n][q], bhi[n][q]);
         }
         int32_t C[NU][2][4];
 #pragma unroll
-        for (int n = 0; n < NU; ++n) dct16<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
+        for (int n = 0; n < NU; ++n) {
+            if (F::H10)
+                dct16h(L, blo[n], bhi[n], C[n]);
+            else
+                dct16<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
+        }
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             // |C| folds into the DFMA operand (fabs of an exact int32 -> double conversion)
@@ -767,11 +906,17 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
         } else {
 #pragma unroll
             for (int n = 0; n < NU; ++n)
-                load4<F, 1>(t < 2 ? boxU[n] : boxU[n] + F::ST_C, ubC[n], g, t & 1, hvC, wvC, XPART, blo[n], bhi[n]);
+                load4<F, 1, F::H10>(t < 2 ? boxU[n] : boxU[n] + F::ST_C, ubC[n], g, t & 1, hvC, wvC, XPART, blo[n],
+                                    bhi[n]);
         }
         int32_t C[NU][4];
 #pragma unroll
-        for (int n = 0; n < NU; ++n) dct8pair<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
+        for (int n = 0; n < NU; ++n) {
+            if (F::H10)
+                dct8pairh(L, blo[n], bhi[n], C[n]);
+            else
+                dct8pair<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
+        }
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             if (ChromaAcc<F>::ON) {
