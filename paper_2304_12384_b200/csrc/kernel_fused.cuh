@@ -65,6 +65,9 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+#ifndef VCA_WAIT_HINT
+#define VCA_WAIT_HINT 1000000
+#endif
 // Blocking wait on an mbarrier phase; the suspend-time hint lets the warp sleep
 // in try_wait until the phase completes instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
@@ -74,7 +77,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
         "VCA_WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
         "@!P bra VCA_WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(parity), "r"(1000000)
+        "r"(parity), "r"(VCA_WAIT_HINT)
         : "memory");
 }
 
@@ -686,11 +689,11 @@ constexpr bool kMmaDownsample = false;
 // Chroma needs only per-frame sums (A7), so a lane may add |C| per coefficient position into
 // exact uint32 accumulators and apply the weight once per flush (every FC units; FC keeps
 // the sums below 2^32: |C| <= (64 n)^2 (2^bd - 1) and FC * that < 2^32) -- no conversion or
-// FP64 op per chroma coefficient, exact sums, only the flushes round.  A/B: +2 % for the
-// n = 16 chroma of the full 32x32 path (16 positions per lane), -2..-5 % for n = 8 chroma
-// (2 positions per lane; the IABS/IADD land on the busiest ALU pipe), so n = 16 only.
+// FP64 op per chroma coefficient, exact sums, only the flushes round.  A/B with the
+// warp-specialised NU = 4 kernel (profiles/r01c/ab_intchroma.log): config 3 +1.9 % burst and
+// +1.7 % under the 1000 W power cap, config 4 +10 %, config 2 +2 % -- on everywhere.
 #ifndef VCA_INT_CHROMA
-#define VCA_INT_CHROMA 1  // 0 never, 1 n = 16 chroma only, 2 always
+#define VCA_INT_CHROMA 2  // 0 never, 1 n = 16 chroma only, 2 always
 #endif
 
 template <class F>
@@ -1033,19 +1036,19 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 //    warpgroups 1..G = consumer groups of 4 warps (setmaxnreg.inc to VCA_CREG), each group
 //    with its own ring, walking its own item sequence exactly like one legacy CTA.
 // Register split (G = 3): producers dec to PREG, consumers inc to CREG <= 128 + (128 - PREG)
-// * 128 / 384.  A/B: 24/160 for the n = 16 luma families (config 3 +1..3 %, config 4 +4 %;
-// the producer loop spills a few bytes), 40/152 for n = 32 (config 2: 160 is -4 %).
+// * 128 / 384.  A/B: 24/160 (the producer loop spills a few bytes) for every family: config 3
+// +1..3 %, config 4 +4 %, config 2 (two n = 32 units per warp) +2 % over 40/152.
 template <class F>
 struct Regs {
 #ifdef VCA_PREG
     static constexpr int P = VCA_PREG;
 #else
-    static constexpr int P = VCA_GROUPS == 3 && F::NY == 16 ? 24 : 40;
+    static constexpr int P = VCA_GROUPS == 3 ? 24 : 40;
 #endif
 #ifdef VCA_CREG
     static constexpr int C = VCA_CREG;
 #else
-    static constexpr int C = VCA_GROUPS == 2 ? 232 : VCA_GROUPS == 3 ? (F::NY == 16 ? 160 : 152) : 104;
+    static constexpr int C = VCA_GROUPS == 2 ? 232 : VCA_GROUPS == 3 ? 160 : 104;
 #endif
 };
 constexpr int kGroups = VCA_GROUPS;

@@ -22,15 +22,21 @@ def main():
     if "--one" not in sys.argv:
         import subprocess
         libs = sys.argv[1:] or sorted(glob.glob(os.path.join(ROOT, "paper_2304_12384_b200", "variants", "*.so")))
-        for rnd in range(2):
+        results = {}
+        for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
             for path in libs:
                 try:
                     r = subprocess.run([sys.executable, __file__, "--one", path, str(rnd)], capture_output=True,
                                        text=True, timeout=int(os.environ.get("AB_TIMEOUT", "120")))
                     sys.stdout.write(r.stdout + (r.stderr[-2000:] if r.returncode else ""))
+                    for line in r.stdout.splitlines():
+                        if " fps " in line:
+                            results.setdefault(os.path.basename(path), []).append(float(line.split()[5]))
                 except subprocess.TimeoutExpired:
                     print("round %d %-28s TIMEOUT" % (rnd, os.path.basename(path)))
                 sys.stdout.flush()
+        for name, v in results.items():
+            print("median %-28s %9.0f fps over %d rounds" % (name, sorted(v)[len(v) // 2], len(v)))
         return
     one(sys.argv[sys.argv.index("--one") + 1], int(sys.argv[-1]))
 
