@@ -88,6 +88,11 @@ class ClockSampler:
         except Exception:
             self.ok = False
             return
+        try:  # board energy counter (mJ) around the timed region
+            self.e0 = float(N.nvmlDeviceGetTotalEnergyConsumption(self.h))
+        except Exception:
+            self.e0 = None
+        self.t0 = time.perf_counter()
         self.stop_flag = False
         self.t = threading.Thread(target=self._run, daemon=True)
         self.t.start()
@@ -110,9 +115,27 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
         self.stop_flag = True
         self.t.join(timeout=2)
+        self.joules = None
+        if self.e0 is not None:
+            try:
+                self.joules = (float(self.N.nvmlDeviceGetTotalEnergyConsumption(self.h)) - self.e0) / 1e3
+                self.seconds = time.perf_counter() - self.t0
+            except Exception:
+                self.joules = None
         sm = sorted(self.samples)
         med = sm[len(sm) // 2] if sm else None
         return {"sm_mhz": med, "sm_max_mhz": self.mx, "reasons": sorted(self.reasons), "samples": len(sm)}
+
+
+def energy_line(clk, frames):
+    """Board energy over the timed region (NVML total-energy counter; this GPU only).  The
+    counter updates every few ms, so short timed regions read coarse values."""
+    if clk is None or getattr(clk, "joules", None) is None or clk.joules <= 0:
+        return None
+    if clk.seconds < 1.0:  # the counter's update interval makes shorter regions meaningless
+        return {"joules": None, "note": "timed region %.3f s < 1 s: run with more --steps for energy" % clk.seconds}
+    return {"joules": clk.joules, "avg_w": clk.joules / clk.seconds, "uj_per_frame": clk.joules / frames * 1e6,
+            "scope": "whole board, this rank's GPU, timed region incl. NVML polling"}
 
 
 def bad_clocks(c):
@@ -258,9 +281,12 @@ def main():
     torch.cuda.synchronize()
     an.profile_read()  # reset counters
 
+    clk_box = [None]
+
     def timed():
         an.profile_enable(True)
         clk = ClockSampler(local)
+        clk_box[0] = clk
         clk.start()
         if world > 1:
             dist.barrier()
@@ -315,6 +341,7 @@ def main():
                      "roofline_fps": peak * 1e9 / fb},
         "gpu_launches": int(launches),
         "clocks": {**clocks, "remeasured": remeasured},
+        "energy": energy_line(clk_box[0], frames_total * args.steps if world == 1 else (nfr - n_halo) * args.steps),
         "paper_context_fps": PAPER_FPS,
     }
 
@@ -336,10 +363,22 @@ def main():
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
+        # context: a plain pinned host -> device copy of the same bytes (the PCIe ceiling)
+        dst = torch.empty(hY.numel() * hY.element_size(), dtype=torch.uint8, device=dev)
+        src = hY.view(torch.uint8).reshape(-1)
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        c0 = time.perf_counter()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_peak = 3 * src.numel() / (time.perf_counter() - c0) / 1e9
+        del dst
         fr = (world if world > 1 else 1) * (ne - n_halo)
         line["e2e"] = {"value": fr * e_steps / dt, "unit": "frames/s", "h2d_bytes_per_step": ne * fb,
                        "d2h_bytes_per_step": (ne - n_halo) * 64, "frames_per_step": ne,
                        "h2d_gbs": ne * fb * e_steps / dt / 1e9 / (world if world > 1 else 1),
+                       "h2d_copy_gbs": h2d_peak,
                        "bound": "PCIe host-to-device copy of the frames (the kernels take < 1 % of the time)",
                        "api": "vca_analyze_host (pinned host memory, 8-frame chunks, copy/compute overlap)"}
         del hY, hU, hV, ae

@@ -368,13 +368,15 @@ int vca_analyze_host(vca_ctx *ctx, const void *const host_planes[3], const int64
     if (chunk_frames > n_frames) chunk_frames = n_frames;
     cudaStream_t user = static_cast<cudaStream_t>(stream);
 
-    // packed device layout of one staged frame: rows of round16(row bytes)
+    // device staging of one chunk, plane-major: [Y frames][U frames][V frames], rows of
+    // round16(row bytes), so a chunk of host frames stored back to back is one 2-D copy per plane
     int64_t dpitch[3], dfs[3], off[3];
     size_t frame_bytes = 0;
     for (int p = 0; p < 3; ++p) {
         dpitch[p] = (((int64_t)ctx->geo[p].width * elem_bytes(ctx)) + 15) & ~(int64_t)15;
-        off[p] = (int64_t)frame_bytes;
-        frame_bytes += (size_t)dpitch[p] * ctx->geo[p].height;
+        dfs[p] = dpitch[p] * ctx->geo[p].height;
+        off[p] = (int64_t)frame_bytes * chunk_frames;
+        frame_bytes += (size_t)dfs[p];
     }
     // (re)allocate context-owned staging when the chunk grows
     const size_t need = frame_bytes * (size_t)chunk_frames;
@@ -438,16 +440,20 @@ int vca_analyze_host(vca_ctx *ctx, const void *const host_planes[3], const int64
         for (int p = 0; p < 3; ++p) {
             const uint8_t *src = static_cast<const uint8_t *>(host_planes[p]) + (int64_t)f0 * frame_stride_bytes[p];
             const size_t wbytes = (size_t)ctx->geo[p].width * elem_bytes(ctx);
-            for (int t = 0; t < m; ++t)
-                VCA_CK(ctx, cudaMemcpy2DAsync(dst + (size_t)t * frame_bytes + off[p], (size_t)dpitch[p],
-                                              src + (int64_t)t * frame_stride_bytes[p], (size_t)pitch_bytes[p], wbytes,
-                                              (size_t)ctx->geo[p].height, cudaMemcpyHostToDevice, ctx->s_copy));
+            const int h = ctx->geo[p].height;
+            if (frame_stride_bytes[p] == pitch_bytes[p] * h)  // frames back to back: one copy of m*h rows
+                VCA_CK(ctx, cudaMemcpy2DAsync(dst + off[p], (size_t)dpitch[p], src, (size_t)pitch_bytes[p], wbytes,
+                                              (size_t)h * m, cudaMemcpyHostToDevice, ctx->s_copy));
+            else
+                for (int t = 0; t < m; ++t)
+                    VCA_CK(ctx, cudaMemcpy2DAsync(dst + off[p] + (size_t)t * dfs[p], (size_t)dpitch[p],
+                                                  src + (int64_t)t * frame_stride_bytes[p], (size_t)pitch_bytes[p],
+                                                  wbytes, (size_t)h, cudaMemcpyHostToDevice, ctx->s_copy));
         }
         VCA_CK(ctx, cudaEventRecord(ctx->ev_copied[b], ctx->s_copy));
         VCA_CK(ctx, cudaStreamWaitEvent(ctx->s_comp, ctx->ev_copied[b], 0));
         const void *dpl[3] = {dst + off[0], dst + off[1], dst + off[2]};
-        int64_t dfstride[3] = {(int64_t)frame_bytes, (int64_t)frame_bytes, (int64_t)frame_bytes};
-        (void)dfs;
+        int64_t dfstride[3] = {dfs[0], dfs[1], dfs[2]};
         const int halo = (f0 == 0) ? n_halo : 0;
         void *scr = static_cast<uint8_t *>(ctx->h_scratch) + (size_t)b * ctx->h_scratch_bytes;
         if (m - halo > 0 || halo) {
