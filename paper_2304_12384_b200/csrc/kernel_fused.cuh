@@ -2,31 +2,31 @@
 // configurations of BASELINE.json: luma block w in {16, 32}, chroma block
 // w/2 on the same block grid, 8- or 10-bit, full or low-pass.
 //
-// One work item = one block row r of one frame f.  A persistent CTA walks its
-// items strip by strip; a strip is 4 horizontally adjacent units, a unit being
-// the co-located Y block (w x w) and U, V blocks (w/2 x w/2) of (f, r, c).
+// One work item = one block row r of one frame f; a unit = the co-located Y block
+// (w x w) and U, V blocks (w/2 x w/2) of (f, r, c); a strip = 4 * NU consecutive units.
+// One persistent CTA per SM, warp-specialised (kGroups = 3):
 //
-//  * warp 0 (one elected lane) is the TMA producer: per strip it issues one
-//    3-D tensor-map load per plane box (swizzled, zero-filled out of bounds)
-//    into a ring of smem stages guarded by full/empty mbarriers (A1);
-//  * warps 1..4 are consumers, warp 1+u owning unit 4s+u of strip s.  A
-//    consumer reads its unit from smem with clamped row/column indices (edge
-//    replication, A2), low-pass-downsamples in registers with
-//    (s+2)>>2 (A3, R-5), and runs the exact integer DCT C = T X T^T on the
-//    tensor cores (A4, R-1) as two int8 IMMA passes that never leave
-//    registers:
-//        pass 1   Z^T = T . X^T      (s8 basis x u8 pixels -> s32)
-//        pass 2   C   = T' . Z'      with Z split into 3 byte planes
+//  * warpgroup 0: producers (setmaxnreg.dec).  Warp g's elected lane feeds consumer
+//    group g: per strip one 3-D tensor-map load per plane box (swizzled, zero-filled out
+//    of bounds) into the group's ring of smem stages, full/empty mbarriers (A1);
+//  * warpgroups 1..3: consumer groups of 4 warps (setmaxnreg.inc), each walking its own
+//    item sequence; warp u owns units u + 4n (n < NU) of every strip.  A consumer reads
+//    its units from smem with clamped row/column indices (edge replication, A2),
+//    low-pass-downsamples in registers with (s+2)>>2 (A3, R-5), and runs the exact
+//    integer DCT C = T X T^T on the tensor cores (A4, R-1) as two passes that never
+//    leave registers:
+//        pass 1   Z^T = T . X^T      (s8 basis x u8 pixels -> s32; 10-bit n = 16/8:
+//                                     f16 x f16 -> f32 with an exact magic offset)
+//        pass 2   C   = T' . Z'      with Z split in three byte planes
 //                 (u8, u8, s8) and C = D0 + 2^8 D1 + 2^16 D2 (mod 2^32);
 //    the C-fragment layout of pass 1 is, up to a fixed permutation pi of the
 //    contraction index y, the B-fragment layout of pass 2, so T' = T[:, pi]
 //    (a constant) absorbs the transpose -- no shuffles, no smem round trip.
-//    10-bit samples enter pass 1 as two byte planes (lo, hi).
 //    Chroma 8x8 DCTs pair U and V block-diagonally into one 16x16 MMA.
-//  * the FP64 epilogue (A5, A6, R-2, R-3) weighs |C_ij| by the
-//    per-lane-constant w_n(i,j)/(4096 n), reduces the luma H per unit (needed
-//    per block for h) and U/V H per item, and writes per-(frame, row, warp)
-//    partial sums in a fixed order (A7 inputs, R-11).
+//  * the epilogue (A5, A6, R-2, R-3): luma |C_ij| x w_n(i,j)/(4096 n) in FP64 per
+//    block (needed per block for h), chroma |C| summed exactly per coefficient
+//    position in uint32 and weighted once per flush; per-(frame, row, warp) partial
+//    sums in a fixed order (A7 inputs, R-11).
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -91,11 +91,7 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
-#ifdef VCA_MMA_NONVOLATILE
-#define VCA_MMA_ASM asm  // pure register op: lets the compiler reorder around it
-#else
-#define VCA_MMA_ASM asm volatile
-#endif
+#define VCA_MMA_ASM asm volatile  // A/B: non-volatile (reorderable) MMA asm was neutral
 // D = A(s8) . B(u8) + C, m16n8k16
 __device__ __forceinline__ void mma16_su(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b)
 {
@@ -299,7 +295,6 @@ __device__ __forceinline__ int box_sample(uint32_t box, int ub0, int row, int xs
 // picks byte 0 of each lane after >> 2 (s >> 2 <= 255, so no masking is needed).
 __device__ __forceinline__ uint32_t ds8(uint2 a, uint2 b)
 {
-#ifndef VCA_DS_ALU
     // 2x2 sums as byte dot products on the FMA pipe (IDP.4A) with weights 64: s' = 64 (s + 2)
     // < 2^16, so byte 1 of s' is (s + 2) >> 2 and three PRMTs pack the four outputs
     const uint32_t s0 = __dp4a(a.x, 0x00004040u, __dp4a(b.x, 0x00004040u, 128u));
@@ -307,12 +302,6 @@ __device__ __forceinline__ uint32_t ds8(uint2 a, uint2 b)
     const uint32_t s2 = __dp4a(a.y, 0x00004040u, __dp4a(b.y, 0x00004040u, 128u));
     const uint32_t s3 = __dp4a(a.y, 0x40400000u, __dp4a(b.y, 0x40400000u, 128u));
     return __byte_perm(__byte_perm(s0, s1, 0x0051), __byte_perm(s2, s3, 0x0051), 0x5410);
-#else
-    const uint32_t M = 0x00FF00FFu;
-    const uint32_t sl = (a.x & M) + __byte_perm(a.x, 0u, 0x4341) + (b.x & M) + __byte_perm(b.x, 0u, 0x4341) + 0x00020002u;
-    const uint32_t sh = (a.y & M) + __byte_perm(a.y, 0u, 0x4341) + (b.y & M) + __byte_perm(b.y, 0u, 0x4341) + 0x00020002u;
-    return __byte_perm(sl >> 2, sh >> 2, 0x6420);
-#endif
 }
 
 // four (2x2 sum + 2) values < 1024 -> packed bytes (s >> 2): low halves paired by PRMT,
@@ -704,11 +693,6 @@ struct ChromaAcc {
     uint32_t u[NP], v[NP];
 };
 
-#ifndef VCA_NO_ACC_CHROMA
-constexpr bool kAccChroma = true;  // chroma |C| FMAs go straight into the running sums (+2 %)
-#else
-constexpr bool kAccChroma = false;
-#endif
 
 template <class F, bool XPART, bool DUMP, int NU>
 __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedArgs &a, const uint32_t (&boxY)[NU],
@@ -720,7 +704,6 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     constexpr int NY = F::NY, NC = F::NC, ES = F::ES;
     const int g = U.g, t = U.t;
     const LaneConst &L = U.L;
-#ifndef VCA_WREG
     // weights from smem ([e][lane] doubles, conflict-free), loaded once per call
     double wl[8], wcc[2];
     if (NY == 16 && NC == 8) {
@@ -734,12 +717,6 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 #pragma unroll
         for (int e = 0; e < 2; ++e) wcc[e] = U.wc[e];
     }
-#define VCA_WL(e) wl[e]
-#define VCA_WC(e) wcc[e]
-#else
-#define VCA_WL(e) U.wl16[e]
-#define VCA_WC(e) U.wc[e]
-#endif
     double hY[NU];
     // 8-bit low-pass on whole columns: the 2x2 sums run on the tensor cores (A3 as an
     // exact 0/1 contraction, rounding offset as the accumulator init)
@@ -791,20 +768,13 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             // |C| folds into the DFMA operand (fabs of an exact int32 -> double conversion)
-#ifdef VCA_SINGLE_CHAIN
-            double h0 = 0.0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) h0 = fma(VCA_WL(e), fabs(i2d(C[n][e >> 2][e & 3])), h0);
-            hY[n] = h0;
-#else
             double h0 = 0.0, h1 = 0.0;  // two FMA chains, combined once (fixed order)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                h0 = fma(VCA_WL(e), fabs(i2d(C[n][0][e])), h0);
-                h1 = fma(VCA_WL(4 + e), fabs(i2d(C[n][1][e])), h1);
+                h0 = fma(wl[e], fabs(i2d(C[n][0][e])), h0);
+                h1 = fma(wl[4 + e], fabs(i2d(C[n][1][e])), h1);
             }
             hY[n] = h0 + h1;
-#endif
             o[n].dcY = C[n][0][0];
             if (DUMP) {
 #pragma unroll
@@ -928,16 +898,12 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                 ca.v[0] += (uint32_t)abs(C[n][2]);
                 ca.v[1] += (uint32_t)abs(C[n][3]);
                 if (DUMP) {
-                    o[n].hu = fma(VCA_WC(1), fabs(i2d(C[n][1])), VCA_WC(0) * fabs(i2d(C[n][0])));
-                    o[n].hv = fma(VCA_WC(1), fabs(i2d(C[n][3])), VCA_WC(0) * fabs(i2d(C[n][2])));
+                    o[n].hu = fma(wcc[1], fabs(i2d(C[n][1])), wcc[0] * fabs(i2d(C[n][0])));
+                    o[n].hv = fma(wcc[1], fabs(i2d(C[n][3])), wcc[0] * fabs(i2d(C[n][2])));
                 }
-            } else if (kAccChroma && !DUMP) {
-                // straight into the warp's running U/V sums (unit order, fixed)
-                hu_acc = fma(VCA_WC(1), fabs(i2d(C[n][1])), fma(VCA_WC(0), fabs(i2d(C[n][0])), hu_acc));
-                hv_acc = fma(VCA_WC(1), fabs(i2d(C[n][3])), fma(VCA_WC(0), fabs(i2d(C[n][2])), hv_acc));
             } else {
-                o[n].hu = fma(VCA_WC(1), fabs(i2d(C[n][1])), VCA_WC(0) * fabs(i2d(C[n][0])));
-                o[n].hv = fma(VCA_WC(1), fabs(i2d(C[n][3])), VCA_WC(0) * fabs(i2d(C[n][2])));
+                o[n].hu = fma(wcc[1], fabs(i2d(C[n][1])), wcc[0] * fabs(i2d(C[n][0])));
+                o[n].hv = fma(wcc[1], fabs(i2d(C[n][3])), wcc[0] * fabs(i2d(C[n][2])));
                 hu_acc += o[n].hu;
                 hv_acc += o[n].hv;
             }
@@ -1234,7 +1200,6 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
             // unit m = s*NU + n of the item goes to stash slot m & 31
             const uint32_t base = smem0 + st * F::STAGE;
             const int c0 = s * F::UNITS + u;
-#ifndef VCA_NULL_COMPUTE
             UnitOut o[NU];
             if (s < s_fast) {
                 uint32_t bY[NU], bU[NU];
@@ -1276,7 +1241,6 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     if (lane == 0) sts<uint4>(sxs + slot * 16, make_uint4(o1[0].dcY, o1[0].dcU, o1[0].dcV, 0u));
                 }
             }
-#endif
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * st);
             if (++st == F::STAGES) {
