@@ -233,3 +233,24 @@ def test_parity_8k_two_frames():
     for lp in (True, False):
         g, r, a = run_both(Y, U, V, 8, 32, lp)
         assert_records(g, r)
+
+
+@pytest.mark.parametrize("mode", ("full", "lowpass"))
+def test_golden_closed_form_gpu(mode):
+    """tests/golden/derived.json (closed form from the definitions) through the
+    CUDA path: E_Y = w* a / n, h = w* |a1 - a0| / n, L = sqrt(v n)."""
+    import json
+    import os
+
+    from test_oracle_pins import _fixture_frames
+
+    g = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                    "derived.json")))["closed_form_frames"][mode]
+    Y, U, V = (torch.from_numpy(p) for p in _fixture_frames((50, 20), mode == "lowpass"))
+    a = Analyzer(Y.shape[2], Y.shape[1], 8, 32, mode == "lowpass")
+    rec = records_to_numpy(a.analyze(*planes_cuda(Y, U, V)))
+    assert rec["E_Y"].tolist() == pytest.approx(g["E_Y"], rel=1e-14)
+    assert rec["h"][0] == 0.0 and rec["h"][1] == pytest.approx(g["h"][1], rel=1e-14)
+    for f in ("L_Y", "L_U", "L_V"):
+        assert rec[f].tolist() == pytest.approx([g[f]] * 2, rel=1e-15)
+    assert np.all(rec["E_U"] == 0.0) and np.all(rec["E_V"] == 0.0)
