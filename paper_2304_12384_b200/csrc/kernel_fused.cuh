@@ -210,11 +210,15 @@ struct Fam {
 #endif
     // units per consumer warp per strip (ILP, per-strip overhead); 4 only while a 16-unit stage
     // stays <= 24 KB (two stages per group, three groups per CTA)
-    static constexpr int NU = (NY != 16) ? VCA_NU32 : (VCA_NU == 4 && 24 * ES * W * W > 24576) ? 2 : VCA_NU;
+    static constexpr int NU = (NY != 16) ? VCA_NU32 : (6 * VCA_NU * ES * W * W > 24576) ? 2 : VCA_NU;
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
-    static constexpr int IB_Y = (UNITS * RB_Y) < 128 ? UNITS * RB_Y : 128;  // box inner bytes = swizzle span
-    static constexpr int IB_C = (UNITS * RB_C) < 128 ? UNITS * RB_C : 128;
+    // box inner bytes = swizzle span: the largest of 128/64/32 bytes that tiles the strip row
+    static constexpr int ib(int row) { return row % 128 == 0 ? 128 : row % 64 == 0 ? 64 : 32; }
+    static constexpr int IB_Y = ib(UNITS * RB_Y);
+    static constexpr int IB_C = ib(UNITS * RB_C);
+    static_assert((UNITS * RB_Y) % IB_Y == 0 && (UNITS * RB_C) % IB_C == 0, "boxes tile the strip");
+    static constexpr int SPF = 32 / NU;  // strips per stash flush (<= 32 units stashed)
     static constexpr int UPB_Y = IB_Y / RB_Y, UPB_C = IB_C / RB_C;        // units per box
     static constexpr int NBOX_Y = UNITS / UPB_Y, NBOX_C = UNITS / UPB_C;
     static constexpr int BOXB_Y = IB_Y * W, BOXB_C = IB_C * WC;            // bytes per box
@@ -222,7 +226,7 @@ struct Fam {
     static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
     static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
 #ifndef VCA_RING
-#define VCA_RING 36864  // 3 stages of 12 KB (config 3); A/B: 3, 4 stages equal, 5 -> 2 CTAs/SM, -16 %
+#define VCA_RING 55296  // ring bytes per consumer group: 3 x 18 KB (NU = 3), 2 x 24 KB (NU = 4)
 #endif
     static constexpr int RING = VCA_RING;  // ring bytes per CTA (several CTAs per SM)
     static constexpr int STAGES = (RING / STAGE) < 2 ? 2 : (RING / STAGE > 16 ? 16 : RING / STAGE);
@@ -1211,9 +1215,9 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     kk[n] = DUMP ? (int64_t)r * cols + c0 + 4 * n : 0;
                 }
                 process_units<F, false, DUMP, NU>(U, a, bY, bU, ubYc, ubCc, hvY, hvC, W, WC, kk, o, hu, hv, ca);
-                // stash: per-unit luma row-group partials and raw C_00 values, reduced 32 units
-                // at a time (NU divides 32, so the strip's slots are consecutive)
-                const uint32_t sl0 = (uint32_t)(s * NU) & 31u;
+                // stash: per-unit luma row-group partials and raw C_00 values, reduced SPF strips
+                // (<= 32 units) at a time
+                const uint32_t sl0 = (uint32_t)((s % F::SPF) * NU);
 #pragma unroll
                 for (int n = 0; n < NU; ++n) {
                     if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, o[n].hY);
@@ -1236,7 +1240,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                         process_units<F, true, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, wvY, wvC, kk, o1, hu, hv, ca);
                     else
                         process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1, hu, hv, ca);
-                    const uint32_t slot = (uint32_t)(s * NU + n) & 31u;
+                    const uint32_t slot = (uint32_t)((s % F::SPF) * NU + n);
                     if (t == 0) sts<double>(hst + (slot * 9 + g) * 8, o1[0].hY);
                     if (lane == 0) sts<uint4>(sxs + slot * 16, make_uint4(o1[0].dcY, o1[0].dcU, o1[0].dcV, 0u));
                 }
@@ -1247,8 +1251,9 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                 st = 0;
                 phase ^= 1;
             }
-            const int mlast = s * NU + NU - 1;  // last unit index of this strip
-            if (ChromaAcc<F>::ON && (((mlast + 1) % ChromaAcc<F>::FC) == 0 || s == strips - 1)) {
+            constexpr int SPC = ChromaAcc<F>::FC / NU;  // strips per chroma flush (<= FC units)
+            static_assert(SPC >= 1, "chroma flush period");
+            if (ChromaAcc<F>::ON && ((s % SPC) == SPC - 1 || s == strips - 1)) {
                 // chroma flush: weight the exact per-position sums once (fixed position order)
 #pragma unroll
                 for (int e = 0; e < ChromaAcc<F>::NP; ++e) {
@@ -1257,14 +1262,15 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     ca.u[e] = ca.v[e] = 0u;
                 }
             }
-            if ((mlast & 31) == 31 || s == strips - 1) {
-                // flush: lane l finishes unit m = mlast - (mlast & 31) + l -- H_Y (fixed order
-                // over the 8 row groups), its L terms (A6), the per-block H_Y store (A5, needed
-                // for h); then a fixed xor tree over lanes into the running item sums.
-                const int m = mlast - (mlast & 31) + lane;
+            if ((s % F::SPF) == F::SPF - 1 || s == strips - 1) {
+                // flush: lane l finishes unit m = first unit of the window + l -- H_Y (fixed
+                // order over the 8 row groups), its L terms (A6), the per-block H_Y store (A5,
+                // needed for h); then a fixed xor tree over lanes into the running item sums.
+                const int nwin = ((s % F::SPF) + 1) * NU;  // units stashed in this window
+                const int m = (s - (s % F::SPF)) * NU + lane;
                 const int cl = (m / NU) * F::UNITS + u + 4 * (m % NU);
                 double Hl = 0.0, LYl = 0.0, LUl = 0.0, LVl = 0.0;
-                if (lane <= (mlast & 31) && cl < cols) {
+                if (lane < nwin && cl < cols) {
 #pragma unroll
                     for (int gg = 0; gg < 8; ++gg) Hl += lds_f64(hst + (lane * 9 + gg) * 8);
                     // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
