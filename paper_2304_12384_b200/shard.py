@@ -59,8 +59,9 @@ def gather_records(local, world: int, group=None, counts=None):
         out = torch.empty((world * m, local.shape[1]), dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(out, pad.contiguous(), group=group)
         parts = [out[i * m: i * m + counts[i]] for i in range(world)]
-    else:
-        bufs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(bufs, pad.contiguous(), group=group)
-        parts = [bufs[i][: counts[i]] for i in range(world)]
+    else:  # gloo: host tensors
+        host = pad.detach().cpu().contiguous()
+        bufs = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(bufs, host, group=group)
+        parts = [bufs[i][: counts[i]].to(local.device) for i in range(world)]
     return torch.cat(parts, dim=0)
