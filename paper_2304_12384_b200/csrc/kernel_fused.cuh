@@ -267,14 +267,33 @@ __device__ __forceinline__ uint32_t smem_off(const void *p)
 {
     return (uint32_t)(reinterpret_cast<const uint8_t *>(p) - vca_dyn_smem);
 }
+#ifdef VCA_DEBUG_BOUNDS
+// debug builds (tests/test_bounds_gpu.py): every data-path shared access is checked against
+// the dynamic shared-memory size and its natural alignment
+__device__ __forceinline__ void smem_check(uint32_t off, uint32_t bytes)
+{
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (off + bytes > dyn || (off & (bytes - 1)) != 0) {
+        printf("VCA_DEBUG_BOUNDS: smem access %u+%u outside [0, %u) or misaligned (block %d thread %d)\n", off, bytes,
+               dyn, blockIdx.x, threadIdx.x);
+        __trap();
+    }
+}
+#define VCA_SMEM_CHECK(off, T) smem_check(off, sizeof(T))
+#else
+#define VCA_SMEM_CHECK(off, T) ((void)0)
+#endif
 template <class T>
 __device__ __forceinline__ T lds(uint32_t off)
 {
+    VCA_SMEM_CHECK(off, T);
     return *reinterpret_cast<const T *>(vca_dyn_smem + off);
 }
 template <class T>
 __device__ __forceinline__ void sts(uint32_t off, T v)
 {
+    VCA_SMEM_CHECK(off, T);
     *reinterpret_cast<T *>(vca_dyn_smem + off) = v;
 }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) { return lds<uint8_t>(a); }
@@ -1278,6 +1297,9 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     LYl = sqrt((double)(dc.x >> 12) * invNY);
                     LUl = sqrt((double)(dc.y >> 12) * invNC);
                     LVl = sqrt((double)(dc.z >> 12) * invNC);
+#ifdef VCA_DEBUG_BOUNDS
+                    if (cl < 0 || cl >= cols) __trap();
+#endif
                     HYrow[cl] = Hl;
                 }
 #pragma unroll
