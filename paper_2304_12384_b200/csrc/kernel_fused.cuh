@@ -210,7 +210,9 @@ struct Fam {
 #endif
     // units per consumer warp per strip (ILP, per-strip overhead); 4 only while a 16-unit stage
     // stays <= 24 KB (two stages per group, three groups per CTA)
-    static constexpr int NU = (NY != 16) ? VCA_NU32 : (6 * VCA_NU * ES * W * W > 24576) ? 2 : VCA_NU;
+    static constexpr int NU = NY == 32  ? VCA_NU32
+                              : NY == 8 ? 4  // n = 8 luma pairs + one 8-block n = 4 chroma MMA per warp
+                              : (6 * VCA_NU * ES * W * W > 24576) ? 2 : VCA_NU;
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
     // box inner bytes = swizzle span: the largest of 128/64/32 bytes that tiles the strip row
@@ -221,10 +223,13 @@ struct Fam {
     static constexpr int SPF = 32 / NU;  // strips per stash flush (<= 32 units stashed)
     static constexpr int UPB_Y = IB_Y / RB_Y, UPB_C = IB_C / RB_C;        // units per box
     static constexpr int NBOX_Y = UNITS / UPB_Y, NBOX_C = UNITS / UPB_C;
-    static constexpr int BOXB_Y = IB_Y * W, BOXB_C = IB_C * WC;            // bytes per box
+    // smem stride per box: whole swizzle atoms (8 rows x IB bytes), so every box starts at an
+    // atom-aligned address and swz() (relative to the box) matches the TMA's absolute pattern
+    // (chroma boxes of the w = 8 family have only 4 rows)
+    static constexpr int BOXB_Y = IB_Y * (W < 8 ? 8 : W), BOXB_C = IB_C * (WC < 8 ? 8 : WC);
     static constexpr int ST_Y = NBOX_Y * BOXB_Y, ST_C = NBOX_C * BOXB_C;
-    static constexpr int TX = ST_Y + 2 * ST_C;                              // bytes landing per stage
-    static constexpr int STAGE = (TX + 1023) / 1024 * 1024;
+    static constexpr int TX = NBOX_Y * IB_Y * W + 2 * NBOX_C * IB_C * WC;   // bytes landing per stage
+    static constexpr int STAGE = (ST_Y + 2 * ST_C + 1023) / 1024 * 1024;
 #ifndef VCA_RING
 #define VCA_RING 55296  // ring bytes per consumer group: 3 x 18 KB (NU = 3), 2 x 24 KB (NU = 4)
 #endif
@@ -443,6 +448,9 @@ struct LaneConst {
     // corrections of the pass-2 accumulators (dct16h, dct8pairh)
     uint32_t h16[4], h8[4];
     int32_t dcfix16, dcfix8e, dcfix8o;
+    // n = 4 chroma of the n = 8 families (dct4oct): pass-1 A = blockdiag(T4 x 4) over
+    // (unit, x), pass-2 A = blockdiag over (unit half, plane) with the pi4 slot order
+    uint32_t t4a0, t4a1, p4a0, p4a1;
 };
 
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d)
@@ -457,7 +465,7 @@ __device__ __forceinline__ int pi32(int k) { return 16 * (k >> 4) + pi16(k & 15)
 
 __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all, int g, int t, int NY)
 {
-    if (NY == 16 || NY == 32) {
+    if (NY == 8 || NY == 16 || NY == 32) {
         const int8_t *T16 = T_all + table_offset(16);
         const int8_t *T8 = T_all + table_offset(8);
         auto T16a = [&](int i, int x) { return (int)__ldg(T16 + i * 16 + x); };
@@ -490,6 +498,27 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
             if (2 * t + (i >> 1) == g) r |= 1u << (8 * i);
         L.rl = r;
         L.rc = r;
+    }
+    if (NY == 8) {
+        // dct4oct.  Pass 1: row m = (b = m >> 2, j = m & 3), slot k = 4t + i = (b' = t, x = i):
+        // A = T4[j][x] if b == b'.  Pass 2: row m' = (beta' = m' >> 3, c' = (m' >> 2) & 1, i' = m' & 3),
+        // slot k' = 4t + i = (beta = i >> 1, c = t >> 1, y = 2 (t & 1) + (i & 1)):
+        // A' = T4[i'][y] if beta' == beta and c' == c.  Lane rows are g (a0) and g + 8 (a1).
+        const int8_t *T4 = T_all + table_offset(4);
+        auto T4a = [&](int i, int x) { return (int)__ldg(T4 + i * 4 + x); };
+        int v0[4], v1[4], w0[4], w1[4];
+        for (int i = 0; i < 4; ++i) {
+            v0[i] = t == (g >> 2) ? T4a(g & 3, i) : 0;
+            v1[i] = t == 2 + (g >> 2) ? T4a(g & 3, i) : 0;
+            const int y = 2 * (t & 1) + (i & 1);
+            const bool cmatch = (t >> 1) == (g >> 2);
+            w0[i] = (cmatch && (i >> 1) == 0) ? T4a(g & 3, y) : 0;
+            w1[i] = (cmatch && (i >> 1) == 1) ? T4a(g & 3, y) : 0;
+        }
+        L.t4a0 = pack4(v0[0], v0[1], v0[2], v0[3]);
+        L.t4a1 = pack4(v1[0], v1[1], v1[2], v1[3]);
+        L.p4a0 = pack4(w0[0], w0[1], w0[2], w0[3]);
+        L.p4a1 = pack4(w1[0], w1[1], w1[2], w1[3]);
     }
     if (NY == 16) {
         // f16 A fragment (m16n8k16, row-major): reg 0 = A[g][2t, 2t+1], 1 = A[g+8][2t, 2t+1],
@@ -659,6 +688,30 @@ __device__ __forceinline__ void dct8pairh(const LaneConst &L, uint32_t blo, uint
     for (int e = 0; e < 4; ++e) C[e] = combine3(E0[e], E1[e], E2[e]);
 }
 
+// n = 4 chroma of 4 units x {U, V} = 8 blocks in one pass-1 and three pass-2 MMAs.  B fragment:
+// lane (g, t) holds 4 samples x = 0..3 of row g & 3 of unit t's plane g >> 2 (U, V).  Output
+// C[e]: plane g >> 2, i = g & 3, j = 2 (t & 1) + (e & 1), unit t >> 1 (e < 2) or 2 + (t >> 1).
+template <int ES>
+__device__ __forceinline__ void dct4oct(const LaneConst &L, uint32_t blo, uint32_t bhi, int32_t (&C)[4])
+{
+    int32_t D1[4];
+    mma16_su(D1, L.t4a0, L.t4a1, blo);
+    if (ES == 2) {
+        int32_t Dh[4];
+        mma16_su(Dh, L.t4a0, L.t4a1, bhi);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) D1[e] = (int32_t)((uint32_t)D1[e] + ((uint32_t)Dh[e] << 8));
+    }
+    uint32_t b0, b1, b2;
+    byte_planes(D1[0], D1[1], D1[2], D1[3], b0, b1, b2);
+    int32_t E0[4], E1[4], E2[4];
+    mma16_su(E0, L.p4a0, L.p4a1, b0);
+    mma16_su(E1, L.p4a0, L.p4a1, b1);
+    mma16_ss(E2, L.p4a0, L.p4a1, b2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) C[e] = combine3(E0[e], E1[e], E2[e]);
+}
+
 // ------------------------------------------------------------------ kernel
 struct FusedArgs {
     int n_frames;
@@ -676,7 +729,8 @@ struct UnitCtx {
     static constexpr int NWC = F::NC == 16 ? 8 : 2;
     LaneConst L;
     double wl16[8];     // luma n = 16 weights at this lane's 8 positions
-    double wc[NWC];     // chroma weights at this lane's positions
+    double wc[NWC];     // chroma weights at this lane's positions (NY = 8: the n = 8 luma pair's)
+    double w4[2];       // NY = 8: n = 4 chroma weights at this lane's positions (dct4oct)
     uint32_t wtab;      // smem offset of this lane's luma n = 32 weights ([pair][lane] double2)
     uint32_t wsm;       // smem address of this lane's n = 16 / 8 weights ([e][lane])
     int g, t;
@@ -1017,6 +1071,119 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     }
 }
 
+// A2-A6 for the n = 8 families (w = 16 low-pass, w = 8 full): one consumer warp's 4 units of
+// a strip.  Luma: two dct8pair calls (units 0|1 and 2|3 as the block-diagonal pair); chroma:
+// one dct4oct for the 4 units x {U, V}.  Lane geometry (which unit a lane loads) is in LY*/LC*.
+// XPART: per-lane valid widths (partial last block column; units past the frame read the
+// zero-filled TMA box and are never stored).  Outputs: per-unit luma row-group partials hY
+// (valid in lanes t == 0), the DC terms (luma in lane 0, chroma in the lanes holding them),
+// exact chroma sums into ca.
+template <class F, bool XPART, bool DUMP>
+__device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedArgs &a, uint32_t base,
+                                               const uint32_t (&LYoff)[2], const int (&LYub)[2], uint32_t LCoff,
+                                               int LCub, int hvY, int hvC, const int (&wvY)[2], int wvC,
+                                               const int64_t (&k)[4], double (&hY)[4], int32_t (&dcY)[4],
+                                               int32_t (&dcC)[2], ChromaAcc<F> &ca)
+{
+    constexpr int ES = F::ES, W = F::W, WC = F::WC;
+    const int g = U.g, t = U.t;
+    const LaneConst &L = U.L;
+    const double wc0 = U.wc[0], wc1 = U.wc[1];
+    // ---- luma: pairs p = 0 (units 0, 1), 1 (units 2, 3); lane t < 2 loads the first unit
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        uint32_t lo, hi;
+        load4<F, 0>(base + LYoff[p], LYub[p], g, t & 1, hvY, XPART ? wvY[p] : W, XPART && wvY[p] < W, lo, hi);
+        int32_t C[4];
+        dct8pair<ES>(L, lo, hi, C);
+        double h0 = fma(wc1, fabs(i2d(C[1])), wc0 * fabs(i2d(C[0])));
+        double h1 = fma(wc1, fabs(i2d(C[3])), wc0 * fabs(i2d(C[2])));
+        h0 += __shfl_xor_sync(0xffffffffu, h0, 1);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+        h0 += __shfl_xor_sync(0xffffffffu, h0, 2);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+        hY[2 * p] = h0;
+        hY[2 * p + 1] = h1;
+        dcY[2 * p] = C[0];
+        dcY[2 * p + 1] = C[2];
+        if (DUMP) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t kk = k[2 * p + (e >> 1)];
+                if (kk >= 0) a.dump.coeffs[0][kk * 64 + g * 8 + 2 * t + (e & 1)] = C[e];
+            }
+        }
+    }
+    // ---- chroma: 8 blocks of 4 x 4 (unit t, plane g >> 2, row g & 3)
+    {
+        uint32_t lo, hi;
+        load4<F, 1>(base + LCoff, LCub, g & 3, 0, hvC, XPART ? wvC : WC, XPART && wvC < WC, lo, hi);
+        int32_t C[4];
+        dct4oct<ES>(L, lo, hi, C);
+        // lane's plane is fixed (g >> 2); slots e and e + 2 share a weight (different units)
+        const uint32_t s0 = (uint32_t)abs(C[0]) + (uint32_t)abs(C[2]);
+        const uint32_t s1 = (uint32_t)abs(C[1]) + (uint32_t)abs(C[3]);
+        if (g < 4) {
+            ca.u[0] += s0;
+            ca.u[1] += s1;
+        } else {
+            ca.v[0] += s0;
+            ca.v[1] += s1;
+        }
+        dcC[0] = C[0];
+        dcC[1] = C[2];
+        if (DUMP) {
+            const int pl = 1 + (g >> 2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t kk = k[e < 2 ? (t >> 1) : 2 + (t >> 1)];
+                if (kk >= 0) a.dump.coeffs[pl][kk * 16 + (g & 3) * 4 + 2 * (t & 1) + (e & 1)] = C[e];
+            }
+            // per-block chroma H: this lane's weighted terms, reduced over the warp per (unit, plane)
+#pragma unroll
+            for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    double v = 0.0;
+                    if ((g >> 2) == q) {
+                        if ((t >> 1) == n) v = fma(U.w4[1], fabs(i2d(C[1])), U.w4[0] * fabs(i2d(C[0])));
+                        if (2 + (t >> 1) == n) v = fma(U.w4[1], fabs(i2d(C[3])), U.w4[0] * fabs(i2d(C[2])));
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if ((g | t) == 0 && k[n] >= 0) a.dump.H[1 + q][k[n]] = v;
+                }
+            // per-block chroma DC sums and L (lane (4q, 2 (n & 1)) holds unit n's plane-q DC)
+            if ((g & 3) == 0 && (t & 1) == 0) {
+                const int q = g >> 2;
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    const int n = m == 0 ? (t >> 1) : 2 + (t >> 1);
+                    if (k[n] >= 0) {
+                        const uint32_t sx = (uint32_t)dcC[m] >> 12;
+                        a.dump.sumx[1 + q][k[n]] = sx;
+                        a.dump.L[1 + q][k[n]] = sqrt((double)sx * (1.0 / F::NC));
+                    }
+                }
+            }
+        }
+    }
+    if (DUMP) {  // per-block luma H, DC sum, L
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            double v = hY[n];
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((g | t) == 0 && k[n] >= 0) {
+                const uint32_t sx = (uint32_t)dcY[n] >> 12;
+                a.dump.H[0][k[n]] = v;
+                a.dump.sumx[0][k[n]] = sx;
+                a.dump.L[0][k[n]] = sqrt((double)sx * (1.0 / F::NY));
+            }
+        }
+    }
+}
+
 // CTA layouts.
 //  * kGroups == 0: 160 threads = 1 producer warp + 4 consumer warps (A/B: a producer-less
 //    ring refilled by the last releasing warp lost 16 %), MINB CTAs per SM.
@@ -1169,6 +1336,9 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
 #pragma unroll
         for (int e = 0; e < UnitCtx<F>::NWC; ++e)
             U.wc[e] = NC == 16 ? U.wl16[e] : __ldg(W8 + g * 8 + 2 * t + e);
+        const double *W4 = a.W_all + table_offset(4);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) U.w4[e] = __ldg(W4 + (g & 3) * 4 + 2 * (t & 1) + e);
     }
     U.wtab = smem_off(wtab) + lane * 16;
     {
@@ -1203,6 +1373,21 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
         ubYc[n] = v % F::UPB_Y;
         ubCc[n] = v % F::UPB_C;
     }
+    // NY = 8 lane geometry: the unit this lane loads for luma pair p (units 2p | 2p + 1, lane
+    // t < 2 -> first) and for the 8-block chroma MMA (unit t, plane g >> 2)
+    uint32_t LYoff[2] = {0u, 0u}, LCoff = 0u;
+    int LYub[2] = {0, 0}, LCub = 0;
+    if (NY == 8) {
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int v = u + 4 * (2 * p + (t >> 1));
+            LYoff[p] = (v / F::UPB_Y) * F::BOXB_Y;
+            LYub[p] = v % F::UPB_Y;
+        }
+        const int v = u + 4 * t;
+        LCoff = F::ST_Y + (v / F::UPB_C) * F::BOXB_C + (g >= 4 ? F::ST_C : 0);
+        LCub = v % F::UPB_C;
+    }
     const int cols_whole = (a.width[0] % W) ? cols - 1 : cols;
     const int last_c = u + 4 * (NU - 1);  // c of this warp's last unit in strip 0
     const int s_fast = cols_whole > last_c ? (cols_whole - last_c - 1) / F::UNITS + 1 : 0;
@@ -1224,7 +1409,37 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
             const uint32_t base = smem0 + st * F::STAGE;
             const int c0 = s * F::UNITS + u;
             UnitOut o[NU];
-            if (s < s_fast) {
+            if (NY == 8) {
+                // n = 8 families: always the 4-unit group path (whole strips without clamps)
+                double hY4[4];
+                int32_t dY[4], dC[2];
+                int64_t kk[4];
+#pragma unroll
+                for (int n = 0; n < 4; ++n) kk[n] = (DUMP && c0 + 4 * n < cols) ? (int64_t)r * cols + c0 + 4 * n : -1;
+                if (s < s_fast) {
+                    const int wY[2] = {W, W};
+                    process_group8<F, false, DUMP>(U, a, base, LYoff, LYub, LCoff, LCub, hvY, hvC, wY, WC, kk, hY4,
+                                                   dY, dC, ca);
+                } else {
+                    int wY[2];
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+                        wY[p] = max(1, min(W, a.width[0] - (c0 + 4 * (2 * p + (t >> 1))) * W));
+                    const int wC = max(1, min(WC, a.width[1] - (c0 + 4 * t) * WC));
+                    process_group8<F, true, DUMP>(U, a, base, LYoff, LYub, LCoff, LCub, hvY, hvC, wY, wC, kk, hY4,
+                                                  dY, dC, ca);
+                }
+                const uint32_t sl0 = (uint32_t)((s % F::SPF) * NU);
+#pragma unroll
+                for (int n = 0; n < 4; ++n) {
+                    if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, hY4[n]);
+                    if (lane == 0) sts<uint32_t>(sxs + (sl0 + n) * 16, (uint32_t)dY[n]);
+                }
+                if ((g & 3) == 0 && (t & 1) == 0) {  // chroma DCs: units t >> 1 and 2 + (t >> 1), plane g >> 2
+                    sts<uint32_t>(sxs + (sl0 + (t >> 1)) * 16 + 4 * (1 + (g >> 2)), (uint32_t)dC[0]);
+                    sts<uint32_t>(sxs + (sl0 + 2 + (t >> 1)) * 16 + 4 * (1 + (g >> 2)), (uint32_t)dC[1]);
+                }
+            } else if (s < s_fast) {
                 uint32_t bY[NU], bU[NU];
                 int64_t kk[NU];
 #pragma unroll
@@ -1276,8 +1491,9 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                 // chroma flush: weight the exact per-position sums once (fixed position order)
 #pragma unroll
                 for (int e = 0; e < ChromaAcc<F>::NP; ++e) {
-                    hu = fma(U.wc[e], __uint2double_rn(ca.u[e]), hu);
-                    hv = fma(U.wc[e], __uint2double_rn(ca.v[e]), hv);
+                    const double wce = NY == 8 ? U.w4[e] : U.wc[e];
+                    hu = fma(wce, __uint2double_rn(ca.u[e]), hu);
+                    hv = fma(wce, __uint2double_rn(ca.v[e]), hv);
                     ca.u[e] = ca.v[e] = 0u;
                 }
             }
@@ -1340,7 +1556,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
 // ------------------------------------------------------------------ host side
 inline bool fused_supported(int w, int lowpass, bool grids_equal)
 {
-    return grids_equal && (w == 32 || (w == 16 && !lowpass));
+    return grids_equal && (w == 32 || w == 16 || (w == 8 && !lowpass));
 }
 inline int fused_partials_per_row() { return 4; }
 
@@ -1393,6 +1609,8 @@ inline cudaError_t fused_prepare(int bd, int lowpass, int w)
 {
     if (w == 32 && lowpass) return bd == 8 ? prepare_one<32, 8, 1>() : prepare_one<32, 10, 1>();
     if (w == 32) return bd == 8 ? prepare_one<32, 8, 0>() : prepare_one<32, 10, 0>();
+    if (w == 16 && lowpass) return bd == 8 ? prepare_one<16, 8, 1>() : prepare_one<16, 10, 1>();
+    if (w == 8) return bd == 8 ? prepare_one<8, 8, 0>() : prepare_one<8, 10, 0>();
     return bd == 8 ? prepare_one<16, 8, 0>() : prepare_one<16, 10, 0>();
 }
 
@@ -1444,6 +1662,12 @@ inline int launch_fused(const Planes3 &pl, int n_frames, int bd, int lowpass, co
     if (w == 32)
         return bd == 8 ? launch_one<32, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
                        : launch_one<32, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+    if (w == 16 && lowpass)
+        return bd == 8 ? launch_one<16, 8, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st)
+                       : launch_one<16, 10, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+    if (w == 8)
+        return bd == 8 ? launch_one<8, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
+                       : launch_one<8, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
     return bd == 8 ? launch_one<16, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
                    : launch_one<16, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
 }

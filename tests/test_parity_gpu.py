@@ -90,6 +90,11 @@ CASES_STRIPS = [
     ("strips_full32", 602, 76, 8, 32, False),          # 19 cols: 2 x 8 + 3, last col 26/32 wide
     ("strips_lp32_10bit", 602, 68, 10, 32, True),      # 19 cols (8-unit strips)
     ("strips_full16_8bit", 1040, 40, 8, 16, False),    # 65 cols: 4 x 16 + 1
+    # n = 8 luma / n = 4 chroma families (luma pairs + 8-block chroma MMA per warp)
+    ("strips_lp16", 586, 70, 8, 16, True),             # 37 cols: 2 x 16 + 5, last col 10/16, last row 6/16
+    ("strips_lp16_10bit", 586, 40, 10, 16, True),
+    ("strips_full8", 294, 30, 8, 8, False),            # 37 cols, last col 6/8 wide, last row 6/8
+    ("strips_full8_10bit", 294, 22, 10, 8, False),
 ]
 
 
