@@ -28,7 +28,8 @@ NVCC_FLAGS = [
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh"))
-                  + glob.glob(os.path.join(CSRC, "*.cpp")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
+                  + glob.glob(os.path.join(CSRC, "*.cpp")) + glob.glob(os.path.join(CSRC, "*.c"))
+                  + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
 def stale() -> bool:
@@ -57,7 +58,24 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     if verbose:
         sys.stderr.write(res.stderr)
     os.replace(tmp, target)
+    if out is None:
+        build_cli()
     return target
+
+
+CLI = os.path.join(HERE, "vca_cli")
+
+
+def build_cli() -> str:
+    """The native C client of the ABI (csrc/vca_cli.c), linked against the in-tree libvca.so."""
+    cmd = ["gcc", "-O2", "-Wall", "-o", CLI + ".tmp", os.path.join(CSRC, "vca_cli.c"), "-L", HERE, "-lvca",
+           "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("gcc failed building vca_cli")
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
 
 
 if __name__ == "__main__":

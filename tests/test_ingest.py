@@ -296,3 +296,23 @@ def test_cli_input_errors(tmp_path):
     bad.write_bytes(b"JUNK W8 H8\n")
     r = cli("analyze", str(bad))
     assert r.returncode == 2 and "MALFORMED_MAGIC" in r.stderr
+
+
+# ---------------------------------------------------------------- native C client of the ABI
+def native_cli(*args):
+    from paper_2304_12384_b200 import build
+
+    if not os.path.exists(build.CLI):
+        build.build_cli()
+    return subprocess.run([build.CLI, *args], capture_output=True, text=True, timeout=300)
+
+
+def test_native_cli_usage_and_input_errors(tmp_path):
+    assert native_cli().returncode == 1
+    assert native_cli("a.yuv").returncode == 1                     # raw without geometry
+    assert native_cli("a.y4m", "--bogus").returncode == 1
+    assert native_cli(str(tmp_path / "missing.y4m")).returncode == 2
+    bad = tmp_path / "bad.y4m"
+    bad.write_bytes(b"JUNK W8 H8\n")
+    r = native_cli(str(bad))
+    assert r.returncode == 2 and "Y4M" in r.stderr

@@ -115,3 +115,18 @@ def test_cli_constant_clip(tmp_path):
     assert len(back) == 3
     for k in ("E_Y", "h", "E_U", "E_V"):
         assert np.all(back[k] == 0.0)
+
+
+def test_native_cli_matches_python_cli(tmp_path):
+    """The plain-C client (csrc/vca_cli.c, no Python/PyTorch) writes the same CSV bytes."""
+    from test_ingest import native_cli
+
+    W, H = 264, 176
+    planes = gen(7, W, H, 8, seed=23)
+    f = tmp_path / "clip.y4m"
+    f.write_bytes(y4m_bytes(planes, W, H, 8))
+    a, b = tmp_path / "py.csv", tmp_path / "c.csv"
+    assert cli("analyze", str(f), "-o", str(a), "--block-size", "32", "--low-pass").returncode == 0
+    r = native_cli(str(f), "-o", str(b), "--block", "32", "--low-pass", "--batch", "3")
+    assert r.returncode == 0, r.stderr
+    assert a.read_bytes() == b.read_bytes()
