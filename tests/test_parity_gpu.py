@@ -259,3 +259,32 @@ def test_golden_closed_form_gpu(mode):
     for f in ("L_Y", "L_U", "L_V"):
         assert rec[f].tolist() == pytest.approx([g[f]] * 2, rel=1e-15)
     assert np.all(rec["E_U"] == 0.0) and np.all(rec["E_V"] == 0.0)
+
+
+@pytest.mark.parametrize("W,H,bd,w,lp", [
+    (2, 2, 8, 32, False),        # smallest accepted frame (R-12): one partial block per plane
+    (2, 2, 10, 8, False),
+    (16384, 34, 8, 32, True),    # very wide: 512 block columns, 32 strips per row
+    (16384, 34, 10, 16, False),
+    (34, 4096, 8, 32, False),    # very tall: 128 block rows of 2 columns
+    (34, 4096, 8, 8, False),
+])
+def test_parity_extreme_shapes(W, H, bd, w, lp):
+    """Degenerate and extreme aspect ratios: records against the oracle."""
+    Y, U, V = synth.g_frames(29, W, H, 3, bd)
+    g, r, _ = run_both(Y, U, V, bd, w, lp)
+    assert_records(g, r)
+
+
+def test_empty_and_single_frame():
+    """n_frames = 0 is an argument error (EmptyStream); one frame gives one record with
+    h = 0 (S:248)."""
+    from paper_2304_12384_b200 import VcaError
+
+    a = Analyzer(64, 32, 8, 16, False)
+    Y, U, V = synth.g_frames(3, 64, 32, 1, 8)
+    with pytest.raises(VcaError) as e:
+        a.analyze(*(p[:0].cuda() for p in (Y, U, V)))
+    assert e.value.code == -1
+    rec = records_to_numpy(a.analyze(*planes_cuda(Y, U, V)))
+    assert len(rec) == 1 and rec["poc"][0] == 0 and rec["h"][0] == 0.0
