@@ -1421,11 +1421,16 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     process_group8<F, false, DUMP>(U, a, base, LYoff, LYub, LCoff, LCub, hvY, hvC, wY, WC, kk, hY4,
                                                    dY, dC, ca);
                 } else {
+                    // valid width of the unit this lane loads; units past the last column read
+                    // the zero-filled box unclamped (never stored)
                     int wY[2];
 #pragma unroll
-                    for (int p = 0; p < 2; ++p)
-                        wY[p] = max(1, min(W, a.width[0] - (c0 + 4 * (2 * p + (t >> 1))) * W));
-                    const int wC = max(1, min(WC, a.width[1] - (c0 + 4 * t) * WC));
+                    for (int p = 0; p < 2; ++p) {
+                        const int c = c0 + 4 * (2 * p + (t >> 1));
+                        wY[p] = c < cols ? min(W, a.width[0] - c * W) : W;
+                    }
+                    const int cC = c0 + 4 * t;
+                    const int wC = cC < cols ? min(WC, a.width[1] - cC * WC) : WC;
                     process_group8<F, true, DUMP>(U, a, base, LYoff, LYub, LCoff, LCub, hvY, hvC, wY, wC, kk, hY4,
                                                   dY, dC, ca);
                 }
