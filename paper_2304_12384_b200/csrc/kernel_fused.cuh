@@ -246,10 +246,9 @@ struct Fam {
 #ifndef VCA_MINB
 #define VCA_MINB 3
 #endif
-    static constexpr int MINB = VCA_MINB;  // CTAs/SM the register budget is sized for               // luma weights from smem (32 per lane)
-    static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;  // per consumer warp
-    static constexpr int SMEM =
-        1024 /*align slack*/ + STAGES * STAGE + 2 * STAGES * 8 + (WTAB ? 32 * 32 * 8 : 0) + 4 * STASH + 10 * 32 * 8;
+    static constexpr int MINB = VCA_MINB;  // CTAs/SM of the legacy layout (kGroups == 0)
+    // per consumer warp: [32 slots][9] doubles (8 luma row-group partials + pad) + [32][4] DC words
+    static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;
     static_assert(NC == NY / 2, "chroma DCT is half the luma DCT");
     static_assert(IB_Y == 32 || IB_Y == 64 || IB_Y == 128, "swizzle span");
     static_assert(IB_C == 32 || IB_C == 64 || IB_C == 128, "swizzle span");
@@ -721,7 +720,6 @@ struct FusedArgs {
     const int8_t *T_all;
     Scratch s;
     DumpPtrs dump;
-    uint64_t l2_policy_unused;
 };
 
 template <class F>
@@ -1640,7 +1638,6 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     a.T_all = T;
     a.s = s;
     a.dump = dp;
-    a.l2_policy_unused = 0;
     const bool dump = dp.coeffs[0] != nullptr;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
     int per_sm = 1;
