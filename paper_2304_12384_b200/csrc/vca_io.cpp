@@ -13,6 +13,9 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <unistd.h>
+#include <algorithm>
+#include <atomic>
 
 #include "../../include/vca_io.h"
 
@@ -24,6 +27,9 @@ struct vca_reader {
     int warnings = 0;
     int64_t frames = 0;
     bool done = false;
+    // positional mode (regular files of fixed-size frame records): frame t's record starts
+    // at data_off + t * rec_bytes and batches are read by several threads with pread
+    int64_t data_off = -1, rec_bytes = 0, data_off_saved = 0;
 };
 
 namespace {
@@ -126,6 +132,83 @@ int64_t read_payload(vca_reader *r, void *const planes[3], const int64_t pitch[3
         }
     }
     return total;
+}
+
+// pread exactly n bytes at off; returns bytes read
+size_t pread_full(int fd, void *dst, size_t n, int64_t off)
+{
+    size_t got = 0;
+    while (got < n) {
+        const ssize_t k = pread(fd, static_cast<uint8_t *>(dst) + got, n - got, (off_t)(off + (int64_t)got));
+        if (k <= 0) break;
+        got += (size_t)k;
+    }
+    return got;
+}
+
+// Positional batch read: frames [r->frames, r->frames + n) by up to VCA_READ_THREADS (16) threads.  Returns VCA_OK
+// or the error of the first failing frame (*first_bad = its batch index).
+int read_positional(vca_reader *r, int n, void *const planes[3], const int64_t pitch[3], const int64_t fstride[3],
+                    int *first_bad)
+{
+    const int fd = fileno(r->f);
+    const vca_stream_info &in = r->info;
+    std::atomic<int> bad{n};
+    std::atomic<int> code{VCA_OK};
+    auto fail = [&](int t, int rc) {
+        int cur = bad.load();
+        while (t < cur && !bad.compare_exchange_weak(cur, t)) {
+        }
+        if (bad.load() == t) code.store(rc);
+    };
+    static const int kThreads = [] {
+        const char *e = getenv("VCA_READ_THREADS");
+        const int v = e ? atoi(e) : 16;
+        return v < 1 ? 1 : (v > 64 ? 64 : v);
+    }();
+    const int T = std::max(1, std::min(n, kThreads));
+    auto work = [&](int k) {
+        for (int t = k; t < n; t += T) {
+            int64_t off = r->data_off + (r->frames + t) * r->rec_bytes;
+            if (r->y4m) {
+                char m[6];
+                const size_t km = pread_full(fd, m, 6, off);
+                if (km < 6) {
+                    fail(t, VCA_ERR_TRUNCATED_FRAME);
+                    continue;
+                }
+                if (memcmp(m, "FRAME\n", 6) != 0) {
+                    // "FRAME" + parameters: the records are not fixed-size after all
+                    fail(t, memcmp(m, "FRAME", 5) == 0 && m[5] == ' ' ? VCA_IO_EOF : VCA_ERR_MALFORMED_FRAME_MARKER);
+                    continue;
+                }
+                off += 6;
+            }
+            for (int p = 0; p < 3; ++p) {
+                const int w = p ? in.chroma_width : in.width, h = p ? in.chroma_height : in.height;
+                const size_t rb = (size_t)w * in.bytes_per_sample;
+                uint8_t *base = static_cast<uint8_t *>(planes[p]) + (int64_t)t * fstride[p];
+                bool ok = true;
+                if ((size_t)pitch[p] == rb) {
+                    ok = pread_full(fd, base, rb * h, off) == rb * h;
+                } else {
+                    for (int y = 0; y < h && ok; ++y)
+                        ok = pread_full(fd, base + (int64_t)y * pitch[p], rb, off + (int64_t)y * rb) == rb;
+                }
+                if (!ok) {
+                    fail(t, VCA_ERR_TRUNCATED_FRAME);
+                    break;
+                }
+                off += (int64_t)rb * h;
+            }
+        }
+    };
+    std::thread pool[63];
+    for (int k = 1; k < T; ++k) pool[k - 1] = std::thread(work, k);
+    work(0);
+    for (int k = 1; k < T; ++k) pool[k - 1].join();
+    *first_bad = bad.load();
+    return code.load();
 }
 
 }  // namespace
@@ -249,6 +332,10 @@ int vca_y4m_open(const char *path, vca_reader **out, vca_stream_info *info)
         setvbuf(f, nullptr, _IOFBF, 1 << 20);
     }
     vca_reader *r = new vca_reader;
+    if (!is_stdin && in.frame_count >= 0) {  // bare "FRAME\n" markers (checked per frame on read)
+        r->data_off = r->data_off_saved = (int64_t)hlen;
+        r->rec_bytes = 6 + in.frame_bytes;
+    }
     r->f = f;
     r->own = !is_stdin;
     r->y4m = true;
@@ -280,6 +367,8 @@ int vca_raw_open(const char *path, int width, int height, int bit_depth, int chr
         if (sz >= 0) {
             in.frame_count = sz / in.frame_bytes;
             if (sz % in.frame_bytes) r->warnings |= VCA_WARN_TRAILING_BYTES;  // discarded, reported
+            r->data_off = 0;
+            r->rec_bytes = in.frame_bytes;
         }
         setvbuf(f, nullptr, _IOFBF, 1 << 20);
     }
@@ -301,6 +390,34 @@ int vca_reader_read(vca_reader *r, int max_frames, void *const planes[3], const 
     for (int p = 0; p < 3; ++p) {
         const int w = p ? r->info.chroma_width : r->info.width;
         if (!planes[p] || pitch_bytes[p] < (int64_t)w * r->info.bytes_per_sample) return VCA_ERR_INVALID_ARG;
+    }
+    if (r->data_off >= 0 && r->info.frame_count >= 0) {  // regular file: parallel positional reads
+        if (r->done) return VCA_IO_EOF;
+        const int n = (int)std::min<int64_t>(max_frames, r->info.frame_count - r->frames);
+        int first_bad = n;
+        const int rc = n > 0 ? read_positional(r, n, planes, pitch_bytes, frame_stride_bytes, &first_bad) : VCA_OK;
+        if (rc == VCA_IO_EOF) {
+            // frame parameters after a bare-marker prefix: deliver the verified frames and
+            // continue sequentially from the first parameterised record
+            r->frames += first_bad;
+            *n_read = first_bad;
+            r->data_off = -1;
+            r->info.frame_count = -1;
+            if (fseeko(r->f, (off_t)(r->data_off_saved + r->frames * r->rec_bytes), SEEK_SET) != 0) return VCA_ERR_IO;
+            return VCA_OK;
+        }
+        if (rc != VCA_OK) {  // the whole frames before the first bad one are delivered
+            r->frames += first_bad;
+            *n_read = first_bad;
+            return rc;
+        }
+        r->frames += n;
+        *n_read = n;
+        if (n < max_frames) {
+            r->done = true;
+            return VCA_IO_EOF;
+        }
+        return VCA_OK;
     }
     for (int t = 0; t < max_frames; ++t) {
         if (r->done) return VCA_IO_EOF;

@@ -316,3 +316,33 @@ def test_native_cli_usage_and_input_errors(tmp_path):
     bad.write_bytes(b"JUNK W8 H8\n")
     r = native_cli(str(bad))
     assert r.returncode == 2 and "Y4M" in r.stderr
+
+
+def test_y4m_parameterised_markers_with_fixed_size(tmp_path):
+    """A Y4M whose later FRAME markers carry parameters but whose size happens to divide into
+    bare-marker records: the positional reader delivers the verified prefix and continues
+    sequentially (R-15)."""
+    planes = frames_420(4, 16, 8, 8, seed=5)
+    fb = 16 * 8 * 3 // 2
+    head = b"YUV4MPEG2 W16 H8 F25:1 C420jpeg\n"
+    recs = []
+    for t in range(4):
+        marker = b"FRAME\n" if t < 2 else b"FRAME Ip\n"
+        recs.append(marker + b"".join(p[t].tobytes() for p in planes))
+    data = head + b"".join(recs)
+    # append a short junk record so the payload size is a multiple of a bare record (6 + fb):
+    # the reader then starts in positional mode and must fall back at frame 2
+    pad = (6 + fb) - (len(data) - len(head)) % (6 + fb)
+    assert 6 <= pad < 6 + fb
+    data += b"FRAME\n" + bytes(pad - 6)
+    f = tmp_path / "p.y4m"
+    f.write_bytes(data)
+    with vcaio.Reader(str(f), "y4m") as r:
+        got = []
+        while True:
+            rc, fr = r.read(8)
+            got.append(fr)
+            if rc != vcaio.VCA_OK or r.frames >= 4:
+                break
+        Y = np.concatenate([g[0] for g in got])
+    assert np.array_equal(Y[:4], planes[0])
