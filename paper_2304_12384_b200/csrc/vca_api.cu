@@ -191,6 +191,19 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         int64_t blocks = (tasks + kGenericWarps - 1) / kGenericWarps;
         const int64_t cap = (int64_t)ctx->sm_count * 16;
         if (blocks > cap) blocks = cap;
+#ifndef VCA_FORCE_GENERIC
+        if (ctx->geo[0].n == 4 && ctx->geo[1].n == 4 && !ctx->lowpass) {  // w = 4: thread per block
+            const int64_t per_frame = ctx->geo[0].count + ctx->geo[1].count + ctx->geo[2].count;
+            if (per_frame > 0x7fffffff) return VCA_ERR_INVALID_ARG;
+            int64_t tb = (per_frame + 255) / 256;
+            const int64_t tcap = (int64_t)ctx->sm_count * 8;
+            if (tb > tcap) tb = tcap;
+            if (ctx->bd == 8)
+                small_block_kernel<8><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+            else
+                small_block_kernel<10><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+        } else
+#endif
         if (ctx->bd == 8)
             generic_block_kernel<8><<<(unsigned)blocks, 32 * kGenericWarps, 0, st>>>(pl, n_frames, ctx->lowpass,
                                                                                     ctx->d_T, ctx->d_W, s, dp);

@@ -95,6 +95,9 @@ CASES_STRIPS = [
     ("strips_lp16_10bit", 586, 40, 10, 16, True),
     ("strips_full8", 294, 30, 8, 8, False),            # 37 cols, last col 6/8 wide, last row 6/8
     ("strips_full8_10bit", 294, 22, 10, 8, False),
+    # w = 4 (thread-per-block kernel; chroma grid half the luma grid)
+    ("wide_full4", 602, 70, 8, 4, False),
+    ("wide_full4_10bit", 330, 38, 10, 4, False),
 ]
 
 
