@@ -67,7 +67,7 @@ enum { VCA_CHROMA_420 = 0, VCA_CHROMA_422 = 1, VCA_CHROMA_444 = 2 };
 /* Kernel path the context resolved to (informational; there is one CUDA
  * backend, these are its two kernel families): the fused TMA + tensor-core kernel
  * for every block size whose chroma grid equals the luma grid (w = 8, 16, 32; w = 16
- * and 32 also low-pass), the warp-generic CUDA-core kernel for w = 4. */
+ * and 32 also low-pass), a CUDA-core kernel (one thread per 4x4 block) for w = 4. */
 enum { VCA_PATH_FUSED_MMA = 1, VCA_PATH_WARP_GENERIC = 2 };
 
 /* Resolved geometry of a context (vca_get_info). */
