@@ -190,6 +190,9 @@ class Analyzer:
         dev = Y.device
         if out is None:
             out = torch.empty((max(F - n_halo, 0), 8), dtype=torch.float64, device=dev)
+        elif (out.dtype != torch.float64 or out.device != dev or not out.is_contiguous()
+              or out.numel() < 8 * max(F - n_halo, 0)):
+            raise ValueError("out must be a contiguous float64 tensor of at least [n_frames - n_halo, 8] on %s" % dev)
         need = self.scratch_bytes(F)
         if scratch is None:
             if self._scratch is None or self._scratch.numel() < need // 8 + 1 or self._scratch.device != dev:
