@@ -174,6 +174,19 @@ class Analyzer:
     def __exit__(self, *a):
         self.close()
 
+    def _check_planes(self, planes):
+        """The tensors must cover the context's planes (the library trusts the geometry it was
+        created with and would read past a smaller buffer)."""
+        es = 1 if self.info["bit_depth"] == 8 else 2
+        W, H = self.info["width"], self.info["height"]
+        for p, t in enumerate(planes):
+            h, w = (H, W) if p == 0 else (H // 2, W // 2)
+            if t.element_size() != es or t.shape[-2] < h or t.shape[-1] < w:
+                raise ValueError("plane %d: need >= %dx%d samples of %d byte(s), got shape %s dtype %s"
+                                 % (p, w, h, es, tuple(t.shape), t.dtype))
+            if t.dim() == 3 and t.shape[0] != planes[0].shape[0]:
+                raise ValueError("planes disagree on the number of frames")
+
     # -- API
     def scratch_bytes(self, max_frames: int) -> int:
         return int(self._L.vca_scratch_bytes(self._h, max_frames))
@@ -185,6 +198,7 @@ class Analyzer:
         """Device planes -> device records tensor [n_frames - n_halo, 8] (float64 view of vca_features)."""
         import torch
 
+        self._check_planes((Y, U, V))
         ptrs, pitch, fstride = _plane_args((Y, U, V), True)
         F = Y.shape[0] if Y.dim() == 3 else 1
         dev = Y.device
@@ -208,6 +222,7 @@ class Analyzer:
         """Host planes (torch CPU tensors, ideally pinned) -> structured numpy records."""
         import torch
 
+        self._check_planes((Y, U, V))
         ptrs, pitch, fstride = _plane_args((Y, U, V), False)
         F = Y.shape[0] if Y.dim() == 3 else 1
         out = np.zeros(max(F - n_halo, 0), dtype=RECORD_DTYPE)
@@ -227,6 +242,7 @@ class Analyzer:
 
     def debug_dump(self, Y, U, V):
         """TEST-ONLY: coefficients / sums / H / L of every block of one frame (device planes)."""
+        self._check_planes((Y, U, V))
         ptrs, pitch, _ = _plane_args((Y, U, V), True)
         res = []
         cptr, sptr, hptr, lptr = [], [], [], []

@@ -189,9 +189,14 @@ def test_argument_errors_gpu():
     a = Analyzer(64, 64, 8, 32, False)
     Y = torch.zeros((2, 64, 64), dtype=torch.uint8, device="cuda")
     U = torch.zeros((2, 32, 32), dtype=torch.uint8, device="cuda")
+    Ywide = torch.zeros((2, 64, 80), dtype=torch.uint8, device="cuda")
     with pytest.raises(VcaError) as e:
-        a.analyze(Y[:, :, 1:], U, U)           # misaligned base (and pitch < row bytes is not the issue)
-    assert e.value.code in (-6, -1)
+        a.analyze(Ywide[:, :, 1:65], U, U)     # large enough, but the base is not 16-byte aligned
+    assert e.value.code == -6
+    with pytest.raises(ValueError):
+        a.analyze(Y[:, :, 1:], U, U)           # smaller than the context's plane: refused by the binding
+    with pytest.raises(ValueError):
+        a.analyze(Y, U, U, out=torch.empty((1, 8), dtype=torch.float64, device="cuda"))  # records buffer too small
     with pytest.raises(VcaError) as e:
         a.analyze(Y[:1], U[:1], U[:1], n_halo=1)  # n_frames < 1 + n_halo
     assert e.value.code == -1
