@@ -1406,6 +1406,11 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
             // unit m = s*NU + n of the item goes to stash slot m & 31
             const uint32_t base = smem0 + st * F::STAGE;
             const int c0 = s * F::UNITS + u;
+#ifdef VCA_NULL_COMPUTE
+            // memory-pipeline probe (A/B only): consumers touch one word of the stage and
+            // release it -- the TMA ring's own ceiling for this layout
+            if (lds32(base + 4 * lane) == 0xFFFFFFFFu && lane == 32) sHY += 1.0;
+#else
             UnitOut o[NU];
             if (NY == 8) {
                 // n = 8 families: always the 4-unit group path (whole strips without clamps)
@@ -1482,6 +1487,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                     if (lane == 0) sts<uint4>(sxs + slot * 16, make_uint4(o1[0].dcY, o1[0].dcU, o1[0].dcV, 0u));
                 }
             }
+#endif
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * st);
             if (++st == F::STAGES) {
