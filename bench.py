@@ -146,13 +146,13 @@ def bad_clocks(c):
     return False
 
 
-def cpu_oracle_fps(Y, U, V, bd, block, lowpass, target_s=10.0, max_frames=None):
+def cpu_oracle_fps(Y, U, V, bd, block, lowpass, target_s=10.0, max_frames=None, threads=None):
     """Time the CPU oracle (as it stands) on a bounded sample; returns (fps, frames, seconds, cores)."""
     import oracle
 
     from paper_2304_12384_b200 import synth
 
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     npl = synth.as_numpy_planes(Y, U, V)
     F = npl[0].shape[0]
     t0 = time.perf_counter()
@@ -343,6 +343,7 @@ def main():
                    if world > 1 else "single GPU",
                    "l2": "inputs %.2f GB per GPU > 126 MB L2; no flush needed" % (nfr * fb / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "frac_vs_8tbs_spec": achieved / 8000.0,
                      "traffic": None if traffic_pf is None else traffic_pf * nfr,
                      "kernel": "block kernel (A1-A7), CUDA events on the launching stream",
                      "algorithmic_bytes_per_launch": nfr * fb, "peak_source": peak_src,
@@ -399,6 +400,12 @@ def main():
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
                                 "sample": "%d frame analyses (repeated passes over the first %d frames of the same "
                                           "workload), %.1f s, OpenMP over frames" % (n, ns, dt)}
+        # the same oracle on one host thread (BASELINE.md asks for both)
+        fps1, n1, dt1, _ = cpu_oracle_fps(Y[:8].cpu(), U[:8].cpu(), V[:8].cpu(), bd, c.block_size, c.lowpass,
+                                          target_s=5.0, threads=1)
+        line["cpu_baseline_1thread"] = {"value": fps1, "unit": "frames/s", "cores": 1, "kind": "oracle",
+                                        "sample": "%d frame analyses (passes over the first 8 frames), %.1f s"
+                                                  % (n1, dt1)}
     if rank == 0:
         # parity spot check of the timed output (first and last record) is done in tests; here sanity only
         rec = records_to_numpy(gathered[0] if world > 1 else out)
