@@ -296,3 +296,31 @@ def test_empty_and_single_frame():
     assert e.value.code == -1
     rec = records_to_numpy(a.analyze(*planes_cuda(Y, U, V)))
     assert len(rec) == 1 and rec["poc"][0] == 0 and rec["h"][0] == 0.0
+
+
+def test_concurrent_contexts_on_streams():
+    """Two contexts analysing on two CUDA streams at the same time give the same records as
+    one after the other (contexts share no mutable state; S:362 determinism)."""
+    Y, U, V = synth.g_frames(41, 264, 176, 6, 8)
+    Y2, U2, V2 = synth.g_frames(42, 264, 176, 6, 8)
+    d1 = planes_cuda(Y, U, V)
+    d2 = planes_cuda(Y2, U2, V2)
+    seq = []
+    for d in (d1, d2):
+        a = Analyzer(264, 176, 8, 32, True)
+        seq.append(records_to_numpy(a.analyze(*d)))
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    a1, a2 = Analyzer(264, 176, 8, 32, True), Analyzer(264, 176, 8, 32, True)
+    outs = []
+    for _ in range(3):  # several overlapping rounds
+        a1.reset(0)
+        a2.reset(0)
+        with torch.cuda.stream(s1):
+            r1 = a1.analyze(*d1, stream=s1)
+        with torch.cuda.stream(s2):
+            r2 = a2.analyze(*d2, stream=s2)
+        torch.cuda.synchronize()
+        outs.append((records_to_numpy(r1), records_to_numpy(r2)))
+    for r1, r2 in outs:
+        assert r1.tobytes() == seq[0].tobytes() and r2.tobytes() == seq[1].tobytes()

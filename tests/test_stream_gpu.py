@@ -130,3 +130,19 @@ def test_native_cli_matches_python_cli(tmp_path):
     r = native_cli(str(f), "-o", str(b), "--block", "32", "--low-pass", "--batch", "3")
     assert r.returncode == 0, r.stderr
     assert a.read_bytes() == b.read_bytes()
+
+
+def test_native_cli_raw_10bit(tmp_path):
+    """Raw 10-bit little-endian input through the plain-C client vs the device-resident path."""
+    from test_ingest import native_cli
+
+    W, H = 136, 100
+    planes = gen(5, W, H, 10, seed=31)
+    f = tmp_path / "clip.yuv"
+    f.write_bytes(raw_bytes(planes))
+    out = tmp_path / "c.csv"
+    r = native_cli(str(f), "--width", str(W), "--height", str(H), "--bit-depth", "10", "--block", "16", "-o", str(out))
+    assert r.returncode == 0, r.stderr
+    want = tmp_path / "want.csv"
+    vcaio.write_csv(str(want), device_records(planes, 10, 16, False))
+    assert out.read_bytes() == want.read_bytes()
