@@ -205,13 +205,16 @@ struct Fam {
 #ifndef VCA_NU
 #define VCA_NU (VCA_GROUPS == 3 ? 4 : 2)
 #endif
+#ifndef VCA_NU8
+#define VCA_NU8 8  // units per warp per strip, n = 8 families (multiple of 4; A/B: 8 vs 4 +6.5 % 1080p lp16, +17 % 720p w8)
+#endif
 #ifndef VCA_NU32
 #define VCA_NU32 2  // units per consumer warp per strip for the n = 32 luma path (A/B: 1 -> 2 +3 %)
 #endif
     // units per consumer warp per strip (ILP, per-strip overhead); 4 only while a 16-unit stage
     // stays <= 24 KB (two stages per group, three groups per CTA)
     static constexpr int NU = NY == 32  ? VCA_NU32
-                              : NY == 8 ? 4  // n = 8 luma pairs + one 8-block n = 4 chroma MMA per warp
+                              : NY == 8 ? VCA_NU8  // groups of 4: 2 luma pairs + one 8-block chroma MMA
                               : (6 * VCA_NU * ES * W * W > 24576) ? 2 : VCA_NU;
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
@@ -1373,18 +1376,20 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
     }
     // NY = 8 lane geometry: the unit this lane loads for luma pair p (units 2p | 2p + 1, lane
     // t < 2 -> first) and for the 8-block chroma MMA (unit t, plane g >> 2)
-    uint32_t LYoff[2] = {0u, 0u}, LCoff = 0u;
-    int LYub[2] = {0, 0}, LCub = 0;
-    if (NY == 8) {
+    constexpr int M8 = NY == 8 ? NU / 4 : 1;  // 4-unit groups per warp per strip
+    uint32_t LYoff[M8][2], LCoff[M8];
+    int LYub[M8][2], LCub[M8];
+#pragma unroll
+    for (int m = 0; m < M8; ++m) {
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-            const int v = u + 4 * (2 * p + (t >> 1));
-            LYoff[p] = (v / F::UPB_Y) * F::BOXB_Y;
-            LYub[p] = v % F::UPB_Y;
+            const int v = u + 4 * (4 * m + 2 * p + (t >> 1));
+            LYoff[m][p] = (v / F::UPB_Y) * F::BOXB_Y;
+            LYub[m][p] = v % F::UPB_Y;
         }
-        const int v = u + 4 * t;
-        LCoff = F::ST_Y + (v / F::UPB_C) * F::BOXB_C + (g >= 4 ? F::ST_C : 0);
-        LCub = v % F::UPB_C;
+        const int v = u + 4 * (4 * m + t);
+        LCoff[m] = F::ST_Y + (v / F::UPB_C) * F::BOXB_C + (g >= 4 ? F::ST_C : 0);
+        LCub[m] = v % F::UPB_C;
     }
     const int cols_whole = (a.width[0] % W) ? cols - 1 : cols;
     const int last_c = u + 4 * (NU - 1);  // c of this warp's last unit in strip 0
@@ -1414,38 +1419,44 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
             UnitOut o[NU];
             if (NY == 8) {
                 // n = 8 families: always the 4-unit group path (whole strips without clamps)
-                double hY4[4];
-                int32_t dY[4], dC[2];
-                int64_t kk[4];
-#pragma unroll
-                for (int n = 0; n < 4; ++n) kk[n] = (DUMP && c0 + 4 * n < cols) ? (int64_t)r * cols + c0 + 4 * n : -1;
-                if (s < s_fast) {
-                    const int wY[2] = {W, W};
-                    process_group8<F, false, DUMP>(U, a, base, LYoff, LYub, LCoff, LCub, hvY, hvC, wY, WC, kk, hY4,
-                                                   dY, dC, ca);
-                } else {
-                    // valid width of the unit this lane loads; units past the last column read
-                    // the zero-filled box unclamped (never stored)
-                    int wY[2];
-#pragma unroll
-                    for (int p = 0; p < 2; ++p) {
-                        const int c = c0 + 4 * (2 * p + (t >> 1));
-                        wY[p] = c < cols ? min(W, a.width[0] - c * W) : W;
-                    }
-                    const int cC = c0 + 4 * t;
-                    const int wC = cC < cols ? min(WC, a.width[1] - cC * WC) : WC;
-                    process_group8<F, true, DUMP>(U, a, base, LYoff, LYub, LCoff, LCub, hvY, hvC, wY, wC, kk, hY4,
-                                                  dY, dC, ca);
-                }
                 const uint32_t sl0 = (uint32_t)((s % F::SPF) * NU);
 #pragma unroll
-                for (int n = 0; n < 4; ++n) {
-                    if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, hY4[n]);
-                    if (lane == 0) sts<uint32_t>(sxs + (sl0 + n) * 16, (uint32_t)dY[n]);
-                }
-                if ((g & 3) == 0 && (t & 1) == 0) {  // chroma DCs: units t >> 1 and 2 + (t >> 1), plane g >> 2
-                    sts<uint32_t>(sxs + (sl0 + (t >> 1)) * 16 + 4 * (1 + (g >> 2)), (uint32_t)dC[0]);
-                    sts<uint32_t>(sxs + (sl0 + 2 + (t >> 1)) * 16 + 4 * (1 + (g >> 2)), (uint32_t)dC[1]);
+                for (int m = 0; m < M8; ++m) {
+                    const int cm = c0 + 16 * m;  // column of the group's first unit
+                    double hY4[4];
+                    int32_t dY[4], dC[2];
+                    int64_t kk[4];
+#pragma unroll
+                    for (int n = 0; n < 4; ++n)
+                        kk[n] = (DUMP && cm + 4 * n < cols) ? (int64_t)r * cols + cm + 4 * n : -1;
+                    if (s < s_fast) {
+                        const int wY[2] = {W, W};
+                        process_group8<F, false, DUMP>(U, a, base, LYoff[m], LYub[m], LCoff[m], LCub[m], hvY, hvC, wY,
+                                                       WC, kk, hY4, dY, dC, ca);
+                    } else {
+                        // valid width of the unit this lane loads; units past the last column read
+                        // the zero-filled box unclamped (never stored)
+                        int wY[2];
+#pragma unroll
+                        for (int p = 0; p < 2; ++p) {
+                            const int c = cm + 4 * (2 * p + (t >> 1));
+                            wY[p] = c < cols ? min(W, a.width[0] - c * W) : W;
+                        }
+                        const int cC = cm + 4 * t;
+                        const int wC = cC < cols ? min(WC, a.width[1] - cC * WC) : WC;
+                        process_group8<F, true, DUMP>(U, a, base, LYoff[m], LYub[m], LCoff[m], LCub[m], hvY, hvC, wY,
+                                                      wC, kk, hY4, dY, dC, ca);
+                    }
+                    const uint32_t slm = sl0 + 4 * m;
+#pragma unroll
+                    for (int n = 0; n < 4; ++n) {
+                        if (t == 0) sts<double>(hst + ((slm + n) * 9 + g) * 8, hY4[n]);
+                        if (lane == 0) sts<uint32_t>(sxs + (slm + n) * 16, (uint32_t)dY[n]);
+                    }
+                    if ((g & 3) == 0 && (t & 1) == 0) {  // chroma DCs: units t >> 1 and 2 + (t >> 1), plane g >> 2
+                        sts<uint32_t>(sxs + (slm + (t >> 1)) * 16 + 4 * (1 + (g >> 2)), (uint32_t)dC[0]);
+                        sts<uint32_t>(sxs + (slm + 2 + (t >> 1)) * 16 + 4 * (1 + (g >> 2)), (uint32_t)dC[1]);
+                    }
                 }
             } else if (s < s_fast) {
                 uint32_t bY[NU], bU[NU];
