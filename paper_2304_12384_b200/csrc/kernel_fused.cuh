@@ -165,17 +165,6 @@ __device__ __forceinline__ void byte_planes(uint32_t v0, uint32_t v1, uint32_t v
     p2 = __byte_perm(s1, s3, 0x5410);
 }
 
-// |C| as an exact double: 2^52 + u reinterpreted, minus 2^52 (one DADD)
-__device__ __forceinline__ double abs_to_double(int32_t c)
-{
-    const uint32_t u = (uint32_t)(c < 0 ? -c : c);
-#ifndef VCA_CVT_MAGIC
-    return __uint2double_rn(u);  // I2F.F64.U32 on the conversion pipe (A/B: +3 % over the magic DADD)
-#else
-    return __hiloint2double(0x43300000, (int)u) - 4503599627370496.0;
-#endif
-}
-
 // Exact double of an int32 without the conversion pipe (I2F.F64 retires 16 lanes/clk/SM on
 // B200, DADD 64; tools/micro/pipes.cu): with M = 2^52 + 2^51, the double M + c has low word c
 // and high word 0x43380000 + (c >> 31) (one LEA.HI.SX32), and (M + c) - M = c exactly (DADD).
