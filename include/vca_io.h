@@ -36,7 +36,7 @@ enum {
  * VCA_ERR_UNSUPPORTED_CHROMA (mono, unknown C tag) and
  * VCA_ERR_UNSUPPORTED_BIT_DEPTH (C...p9, p12, ...). */
 
-/* Warning bits (vca_reader_warnings), S:84-86, S:74. */
+/* Warning bits (vca_reader_warnings), S:66, S:83. */
 enum {
     VCA_WARN_TRAILING_BYTES = 1,  /* raw file size not a multiple of the frame size: partial frame discarded */
     VCA_WARN_X_TOKENS = 2         /* Y4M X (extension) tokens ignored                                      */
@@ -76,7 +76,7 @@ int vca_y4m_parse_header(const char *bytes, size_t len, vca_stream_info *info, s
  * VCA_ERR_IO if the file cannot be opened; header errors as above. */
 int vca_y4m_open(const char *path, vca_reader **out, vca_stream_info *info);
 
-/* Open a headerless planar raw YUV file (I420/I422/I444, S:70-75) with the
+/* Open a headerless planar raw YUV file (I420/I422/I444, S:62-70) with the
  * caller's geometry: width, height > 0 (even as the chroma format requires),
  * bit_depth 8 or 10.  frame_count = file size / frame_bytes; a trailing
  * partial frame is discarded and flagged VCA_WARN_TRAILING_BYTES (R-14).

@@ -366,7 +366,7 @@ int vca_raw_open(const char *path, int width, int height, int bit_depth, int chr
         const int64_t sz = file_size(f);
         if (sz >= 0) {
             in.frame_count = sz / in.frame_bytes;
-            if (sz % in.frame_bytes) r->warnings |= VCA_WARN_TRAILING_BYTES;  // S:73: discarded, reported
+            if (sz % in.frame_bytes) r->warnings |= VCA_WARN_TRAILING_BYTES;  // S:66: discarded, reported
             r->data_off = 0;
             r->rec_bytes = in.frame_bytes;
         }

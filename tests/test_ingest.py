@@ -37,7 +37,7 @@ def test_header_chroma_tags(tag, chroma, bd):
     cw = 32 if chroma in (420, 422) else 64
     ch = 16 if chroma == 420 else 32
     es = 1 if bd == 8 else 2
-    assert info["frame_bytes"] == (64 * 32 + 2 * cw * ch) * es  # S:85
+    assert info["frame_bytes"] == (64 * 32 + 2 * cw * ch) * es  # S:74
 
 
 def test_header_default_chroma_and_x_tokens():
@@ -94,7 +94,7 @@ def y4m_bytes(planes, w, h, bd, frame_params=b""):
 
 def test_raw_exact_one_frame(tmp_path):
     f = tmp_path / "a.yuv"
-    f.write_bytes(bytes(range(96)))                     # 8x8 4:2:0 8-bit: 64 + 16 + 16 bytes (S:66)
+    f.write_bytes(bytes(range(96)))                     # 8x8 4:2:0 8-bit: 64 + 16 + 16 bytes (S:59)
     with vcaio.Reader(str(f), "raw", 8, 8, 8) as r:
         assert r.info["frame_bytes"] == 96 and r.info["frame_count"] == 1
         rc, (Y, U, V) = r.read(4)
@@ -106,7 +106,7 @@ def test_raw_exact_one_frame(tmp_path):
 
 @pytest.mark.parametrize("size,frames", [(140, 1), (200, 2), (3 * 96, 3), (3 * 96 + 95, 3)])
 def test_raw_trailing_partial_frame(tmp_path, size, frames):
-    """R-14: a trailing partial raw frame is discarded and flagged (S:73), never half-read."""
+    """R-14: a trailing partial raw frame is discarded and flagged (S:66), never half-read."""
     f = tmp_path / "a.yuv"
     f.write_bytes(bytes(i & 255 for i in range(size)))
     with vcaio.Reader(str(f), "raw", 8, 8, 8) as r:
@@ -118,7 +118,7 @@ def test_raw_trailing_partial_frame(tmp_path, size, frames):
 def test_raw_10bit_little_endian(tmp_path):
     f = tmp_path / "a.yuv"
     b = bytearray(192)
-    b[0:2] = bytes([0xBC, 0x02])                        # 700 (S:75)
+    b[0:2] = bytes([0xBC, 0x02])                        # 700 (S:70)
     f.write_bytes(bytes(b))
     with vcaio.Reader(str(f), "raw", 8, 8, 10) as r:
         rc, (Y, U, V) = r.read(1)
