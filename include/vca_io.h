@@ -79,7 +79,7 @@ int vca_y4m_open(const char *path, vca_reader **out, vca_stream_info *info);
 /* Open a headerless planar raw YUV file (I420/I422/I444) with the
  * caller's geometry: width, height > 0 (even as the chroma format requires),
  * bit_depth 8 or 10.  frame_count = file size / frame_bytes; a trailing
- * partial frame is discarded and flagged VCA_WARN_TRAILING_BYTES (S:73, R-14).
+ * partial frame is discarded and flagged VCA_WARN_TRAILING_BYTES (S:66, R-14).
  * Errors: VCA_ERR_IO, VCA_ERR_MALFORMED_HEADER (bad geometry),
  * VCA_ERR_UNSUPPORTED_BIT_DEPTH, VCA_ERR_UNSUPPORTED_CHROMA. */
 int vca_raw_open(const char *path, int width, int height, int bit_depth, int chroma_format, vca_reader **out,
