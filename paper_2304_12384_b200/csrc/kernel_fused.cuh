@@ -143,6 +143,16 @@ __device__ __forceinline__ void mma16_h(float (&d)[4], const uint32_t (&a)[4], u
         : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c));
 }
+// D = A(f16) . B(f16) + C (f32, per element), m16n8k16 -- the 8-bit two-plane pass 2
+__device__ __forceinline__ void mma16_hc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1, float c0, float c1, float c2, float c3)
+{
+    VCA_MMA_ASM(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(c0), "f"(c1), "f"(c2), "f"(c3));
+}
 // pass 2 with a per-lane accumulator init (the corrections of the 10-bit path)
 __device__ __forceinline__ void mma16_su_c(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b, int32_t c0,
                                            int32_t c1, int32_t c2, int32_t c3)
@@ -442,6 +452,16 @@ struct LaneConst {
     // n = 4 chroma of the n = 8 families (dct4oct): pass-1 A = blockdiag(T4 x 4) over
     // (unit, x), pass-2 A = blockdiag over (unit half, plane) with the pi4 slot order
     uint32_t t4a0, t4a1, p4a0, p4a1;
+    // 8-bit two-plane f16 pass 2 (VCA_F16P2, dct16 / dct8pair): f16 A fragments of T16 and of
+    // T8 in the standard contraction order, the pass-1 offset of this lane's row g (0 for the
+    // DC row, 2^17 otherwise) and the hi-plane accumulator inits carrying the offset's
+    // correction of the C_0k (k != 0) row
+    // (the accumulator quads are loaded opaquely, so they stay resident instead of being
+    // rebuilt with 4 moves per MMA; the corrections sit in the combine constants)
+    uint32_t g16[4], g8;
+    int32_t zq[4];      // pass-1 init {off_g, off_g, 2^17, 2^17}, off_g = 0 for g = 0, else 2^17
+    float mq[4];        // pass-2 init 0.75 (bits 0x3F400000)
+    int32_t kL0, kL1, kC0, kC1;  // combine constants -0x7F400000 - r_0 off_k (luma / chroma)
 };
 
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d)
@@ -482,6 +502,30 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
         }
         L.p8a0 = pack4(u[0], u[1], u[2], u[3]);
         L.p8a1 = pack4(v[0], v[1], v[2], v[3]);
+        auto h2 = [](int a, int b) {
+            return (uint32_t)__half_as_ushort(__int2half_rn(a)) | ((uint32_t)__half_as_ushort(__int2half_rn(b)) << 16);
+        };
+        L.g16[0] = h2(T16a(g, 2 * t), T16a(g, 2 * t + 1));
+        L.g16[1] = h2(T16a(g + 8, 2 * t), T16a(g + 8, 2 * t + 1));
+        L.g16[2] = h2(T16a(g, 2 * t + 8), T16a(g, 2 * t + 9));
+        L.g16[3] = h2(T16a(g + 8, 2 * t + 8), T16a(g + 8, 2 * t + 9));
+        L.g8 = h2(T8a(g, 2 * t), T8a(g, 2 * t + 1));
+        const int zoff = g == 0 ? 0 : (1 << 17);
+        // opaque zero: T16[0][0] - 64 (the compiler cannot fold a loaded value)
+        // (four distinct loads, so the four copies stay distinct registers of one quad)
+        const int z0 = T16a(0, 0) - 64;
+        L.zq[0] = zoff + z0;
+        L.zq[1] = zoff + T16a(0, 1) - 64;
+        L.zq[2] = (1 << 17) + T16a(0, 2) - 64;
+        L.zq[3] = (1 << 17) + T16a(0, 3) - 64;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) L.mq[i] = __int_as_float(0x3F400000 + T16a(0, 4 + i) - 64);
+        // correction r_0 off_k of C_0k (r_0 = 64 n: 2^27 for n = 16, 2^26 for n = 8)
+        const int32_t K = (int32_t)(0u - 0x7F400000u) + z0;
+        L.kL0 = (g == 0 && t != 0) ? K - (1 << 27) : K;
+        L.kL1 = g == 0 ? K - (1 << 27) : K;
+        L.kC0 = (g == 0 && t != 0) ? K - (1 << 26) : K;
+        L.kC1 = g == 0 ? K - (1 << 26) : K;
     }
     {
         uint32_t r = 0;
@@ -568,11 +612,50 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
 // -> C[p][e]: i = g + 8(e>>1), j = 8p + 2t + (e&1).
 // PERM1: the B fragments hold x in the pi16 slot order (tensor-core low-pass output),
 // so pass 1 uses the column-permuted basis T16[:, pi16] -- the same constant as pass 2.
+// 8-bit pass 2 as two f16 planes (VCA_F16P2, off: exact and parity-green, but slower).
+// Pass 1 adds off_k = 2^17 to every row k != 0 through its accumulator (the DC row is >= 0
+// already; the paired-n = 8 V rows take it at k = 0 too): with row sums r_k = 0 for k > 0
+// and sum_x |T_kx| <= 64 n, every Z' = Z + off_k lies in [0, 2^18) for n <= 16 and 8-bit x,
+// so byte 0 (lo) and bytes 1-2 (hi < 1024) of Z' are exact f16 subnormals lo * 2^-24,
+// hi * 2^-24, each picked into the pass-2 B fragment by one PRMT (byte 3 of Z' is 0).  The
+// pass-1 C fragment is the f16 B fragment as is (rows -> n, columns y = 2t, 2t+1 (+8) -> k),
+// so A = T in the standard order.  With the f32 accumulator at 0.75 every partial sum is a
+// multiple of 2^-24 in (0, 1): exact, and the result's bits are 0x3F400000 + S.  Then
+// C = S_lo + 2^8 S_hi - r_i off_k = bits_lo + 2^8 bits_hi - 0x7F400000 - r_i off_k (mod 2^32).
+// 4 PRMT + 2 HMMA instead of 7 PRMT + 3 IMMA per 4 values, yet config 3 -5 %, config 2 -14 %
+// (profiles/r01d/ab_f16_pass2_reverted.log): the f32 HMMA costs more than the IMMAs it
+// replaces and the resident accumulator quads add register pressure.
+#ifndef VCA_F16P2
+#define VCA_F16P2 0
+#endif
+
 template <int ES, bool PERM1 = false>
 __device__ __forceinline__ void dct16(const LaneConst &L, const uint32_t (&blo)[2], const uint32_t (&bhi)[2],
                                       int32_t (&C)[2][4])
 {
     int32_t D1[2][4];
+    if (ES == 1 && VCA_F16P2) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            mma16_su_c(D1[q], PERM1 ? L.p16a0 : L.t16a0, PERM1 ? L.p16a1 : L.t16a1, blo[q], L.zq[0], L.zq[1], L.zq[2],
+                       L.zq[3]);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const uint32_t lo0 = __byte_perm(D1[0][2 * p], D1[0][2 * p + 1], 0x7430);
+            const uint32_t lo1 = __byte_perm(D1[1][2 * p], D1[1][2 * p + 1], 0x7430);
+            const uint32_t hi0 = __byte_perm(D1[0][2 * p], D1[0][2 * p + 1], 0x6521);
+            const uint32_t hi1 = __byte_perm(D1[1][2 * p], D1[1][2 * p + 1], 0x6521);
+            float El[4], Eh[4];
+            mma16_hc(El, L.g16[0], L.g16[1], L.g16[2], L.g16[3], lo0, lo1, L.mq[0], L.mq[1], L.mq[2], L.mq[3]);
+            mma16_hc(Eh, L.g16[0], L.g16[1], L.g16[2], L.g16[3], hi0, hi1, L.mq[0], L.mq[1], L.mq[2], L.mq[3]);
+            const int32_t K0 = p == 0 ? L.kL0 : L.kL1, K1 = L.kL1, K2 = (int32_t)(0u - 0x7F400000u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                C[p][e] = (int32_t)(__float_as_uint(Eh[e]) * 256u + __float_as_uint(El[e]) +
+                                    (uint32_t)(e == 0 ? K0 : e == 1 ? K1 : K2));
+        }
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
         if (PERM1)
@@ -605,6 +688,20 @@ template <int ES, bool PERM1 = false>
 __device__ __forceinline__ void dct8pair(const LaneConst &L, uint32_t blo, uint32_t bhi, int32_t (&C)[4])
 {
     int32_t D1[4];
+    if (ES == 1 && VCA_F16P2) {
+        // V rows take the 2^17 offset also at k = 0 (Z_0 + 2^17 < 2^18 for n = 8), so the
+        // pass-1 quad is the luma one; corrections: U C_0k (k != 0), V C_0k (all k)
+        mma16_su_c(D1, PERM1 ? L.p8a0 : L.t8a0, PERM1 ? L.p8a1 : L.t8a1, blo, L.zq[0], L.zq[1], L.zq[2], L.zq[3]);
+        const uint32_t lo0 = __byte_perm(D1[0], D1[1], 0x7430), lo1 = __byte_perm(D1[2], D1[3], 0x7430);
+        const uint32_t hi0 = __byte_perm(D1[0], D1[1], 0x6521), hi1 = __byte_perm(D1[2], D1[3], 0x6521);
+        float El[4], Eh[4];
+        mma16_hc(El, L.g8, 0u, 0u, L.g8, lo0, lo1, L.mq[0], L.mq[1], L.mq[2], L.mq[3]);
+        mma16_hc(Eh, L.g8, 0u, 0u, L.g8, hi0, hi1, L.mq[0], L.mq[1], L.mq[2], L.mq[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            C[e] = (int32_t)(__float_as_uint(Eh[e]) * 256u + __float_as_uint(El[e]) + (uint32_t)(e == 0 ? L.kC0 : L.kC1));
+        return;
+    }
     if (PERM1)
         mma16_su(D1, L.p8a0, L.p8a1, blo);  // slot 4t+i = (U|V by i>>1, x = 2t + (i&1))
     else
