@@ -221,21 +221,53 @@ def test_profile_counters():
 
 @pytest.mark.slow
 @pytest.mark.parametrize("cfg", (2, 3, 4))
-def test_parity_full_size_sampled(cfg):
-    """Full BASELINE.json geometry, analysed in one call over many frames (the
-    launch configuration bench.py times); sampled frames checked against the
-    oracle (records incl. h via a halo frame, and the coefficient dump)."""
+def test_parity_full_size_all_frames(cfg):
+    """Full BASELINE.json geometry and batch, analysed in one call (the launch configuration
+    bench.py times); every record against the oracle (chunks behind a halo frame for h), every
+    feature finite and non-negative, and the coefficient dump of the last frame."""
     c = synth.CONFIGS[cfg]
-    F = 24
+    F = c.n_frames            # the whole BASELINE.json batch in one call, as bench.py times it
     Y, U, V = synth.config_frames(cfg, device="cuda", n_frames=F)
     a = Analyzer(c.width, c.height, c.bit_depth, c.block_size, c.lowpass)
     g = records_to_numpy(a.analyze(Y, U, V))
-    for t in (1, F - 1):
-        npl = synth.as_numpy_planes(Y[t - 1:t + 1], U[t - 1:t + 1], V[t - 1:t + 1])
-        r = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=1, first_poc=t)
-        assert_records(g[t:t + 1], r)
+    assert len(g) == F and np.array_equal(g["poc"], np.arange(F))
+    for f in FEATS:            # properties of every frame: finite, non-negative
+        assert np.all(np.isfinite(g[f])) and np.all(g[f] >= 0.0), f
+    # every frame against the oracle, in host-sized chunks (each behind a one-frame halo for h)
+    step = 40
+    for s in range(0, F, step):
+        e = min(F, s + step)
+        h0 = 1 if s > 0 else 0
+        npl = synth.as_numpy_planes(Y[s - h0:e], U[s - h0:e], V[s - h0:e])
+        r = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=h0, first_poc=s)
+        assert_records(g[s:e], r)
     Yc, Uc, Vc = (p[F - 1:F].cpu() for p in (Y, U, V))
     check_dump(a, Yc, Uc, Vc, c.bit_depth, c.block_size, c.lowpass, frame=0)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world", (2, 4, 8))
+def test_config5_rank_boundary_full_size(world):
+    """Config 5 at full UHD size: the rank that starts at a segment boundary (shard.plan) analyses
+    its first frames behind a one-frame halo taken from the previous segment; its records equal a
+    single call across the boundary bit for bit (GPU-count invariance) and the oracle."""
+    from paper_2304_12384_b200 import shard
+
+    c = synth.CONFIGS[5]
+    sh = shard.plan(c.n_frames, world, 1)
+    k = 4                                             # records checked after the boundary
+    Y, U, V = synth.config_frames(5, device="cuda", n_frames=k + 2, first_t=sh.first_poc - 2)
+    a = Analyzer(c.width, c.height, 8, c.block_size, c.lowpass)
+    a.reset(sh.first_poc - 2)
+    whole = records_to_numpy(a.analyze(Y, U, V))
+    b = Analyzer(c.width, c.height, 8, c.block_size, c.lowpass)
+    b.reset(sh.first_poc)
+    ranked = records_to_numpy(b.analyze(Y[1:], U[1:], V[1:], n_halo=sh.n_halo))
+    assert ranked["poc"][0] == sh.first_poc and ranked.tobytes() == whole[2:].tobytes()
+    npl = synth.as_numpy_planes(Y[1:3].cpu(), U[1:3].cpu(), V[1:3].cpu())
+    r = oracle.analyze(*npl, 8, c.block_size, c.lowpass, n_halo=1, first_poc=sh.first_poc)
+    assert_records(ranked[:1], r)
+    assert ranked["h"][0] > 0.0                       # h across the segment cut, not a restart
 
 
 @pytest.mark.slow
