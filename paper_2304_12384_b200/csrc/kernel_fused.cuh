@@ -214,7 +214,9 @@ struct Fam {
     // stays <= 24 KB (two stages per group, three groups per CTA)
     static constexpr int NU = NY == 32  ? VCA_NU32
                               : NY == 8 ? VCA_NU8  // groups of 4: 2 luma pairs + one 8-block chroma MMA
-                              : (6 * VCA_NU * ES * W * W > 24576) ? 2 : VCA_NU;
+                              : (6 * VCA_NU * ES * W * W > 24576) ? (VCA_GROUPS == 4 ? 1 : 2) : VCA_NU;
+    // (VCA_GROUPS = 4 is an A/B variant only: 16 consumer warps at 112 registers, NU = 3,
+    // 2 x 18 KB stages per group -- 3 % slower on config 3, profiles/r01d/ab_groups4.log)
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
     static constexpr int RB_Y = W * ES, RB_C = WC * ES;    // bytes per unit row
     // box inner bytes = swizzle span: the largest of 128/64/32 bytes that tiles the strip row
