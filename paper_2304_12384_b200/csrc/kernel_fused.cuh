@@ -855,7 +855,13 @@ template <class F>
 struct ChromaAcc {
     static constexpr bool ON = VCA_INT_CHROMA == 2 || (VCA_INT_CHROMA == 1 && F::NC == 16);
     static constexpr int NP = F::NC == 16 ? 8 : 2;  // coefficient positions per lane per plane
-    static constexpr int FC = (F::NC == 16 && F::ES == 2) ? 4 : 16;  // units per flush
+    // units per flush: the largest power of two <= 64 with FC * (64 n)^2 (2^bd - 1) < 2^32
+    // (n = 8 8-bit: 64; n = 8 10-bit and n = 16 8-bit: 16; n = 16 10-bit: 4); the n = 8 families
+    // (several blocks per position per group) keep 16
+    static constexpr uint64_t CMAX = (uint64_t)(64 * F::NC) * (64 * F::NC) * ((1u << F::BD) - 1u);
+    static constexpr uint64_t FCMAX = 4294967295ull / CMAX;
+    static constexpr int FC = F::NY == 8 ? 16 : FCMAX >= 64 ? 64 : FCMAX >= 32 ? 32 : FCMAX >= 16 ? 16 : FCMAX >= 8 ? 8 : 4;
+    static_assert(F::NY == 8 || (uint64_t)FC * CMAX <= 4294967295ull, "chroma sums fit uint32");
     uint32_t u[NP], v[NP];
 };
 
