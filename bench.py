@@ -378,14 +378,15 @@ def main():
         ne = min(args.e2e_frames, nfr)
         hY, hU, hV = (p[:ne].cpu().pin_memory() for p in (Y, U, V))
         ae = Analyzer(W, H, bd, c.block_size, c.lowpass)
-        ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=8)  # warm-up / staging allocation
+        chunk = int(os.environ.get("VCA_E2E_CHUNK", "8"))
+        ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=chunk)  # warm-up / staging allocation
         if world > 1:
             dist.barrier()
         e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
         for _ in range(e_steps):
             ae.reset(first_poc)
-            ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=8)
+            ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=chunk)
         dt = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device=red_dev)
@@ -408,7 +409,7 @@ def main():
                        "h2d_gbs": ne * fb * e_steps / dt / 1e9 / (world if world > 1 else 1),
                        "h2d_copy_gbs": h2d_peak,
                        "bound": "PCIe host-to-device copy of the frames (the kernels take < 1 % of the time)",
-                       "api": "vca_analyze_host (pinned host memory, 8-frame chunks, copy/compute overlap)"}
+                       "api": "vca_analyze_host (pinned host memory, %d-frame chunks, copy/compute overlap)" % chunk}
         del hY, hU, hV, ae
 
     # --- CPU oracle baseline, rank 0 at N = 1 only
