@@ -1385,6 +1385,18 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
                 for (int s = 0; s < strips; ++s) {
                     if (!first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
                     uint8_t *base = smem + st * F::STAGE;
+#ifdef VCA_NULL_MEMORY
+                    // compute-side probe (A/B only): release the stage without loading it --
+                    // the consumers' own ceiling on whatever the ring holds
+                    mbar_arrive(smem_u32(&full[st]));
+                    (void)base;
+                    if (++st == F::STAGES) {
+                        st = 0;
+                        phase ^= 1;
+                        first_pass = false;
+                    }
+                    continue;
+#endif
                     mbar_expect_tx(&full[st], F::TX);
 #pragma unroll
                     for (int b = 0; b < F::NBOX_Y; ++b)
