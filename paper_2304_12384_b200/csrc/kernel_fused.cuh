@@ -204,6 +204,9 @@ struct Fam {
 #ifndef VCA_NU
 #define VCA_NU (VCA_GROUPS == 3 ? 4 : 2)
 #endif
+#ifndef VCA_STAGE_MAX
+#define VCA_STAGE_MAX 24576  // largest n = 16 luma stage (6 NU ES W^2 bytes) before NU falls back to 2
+#endif
 #ifndef VCA_NU8
 #define VCA_NU8 8  // units per warp per strip, n = 8 families (multiple of 4; A/B: 8 vs 4 +6.5 % 1080p lp16, +17 % 720p w8)
 #endif
@@ -214,7 +217,7 @@ struct Fam {
     // stays <= 24 KB (two stages per group, three groups per CTA)
     static constexpr int NU = NY == 32  ? VCA_NU32
                               : NY == 8 ? VCA_NU8  // groups of 4: 2 luma pairs + one 8-block chroma MMA
-                              : (6 * VCA_NU * ES * W * W > 24576) ? (VCA_GROUPS == 4 ? 1 : 2) : VCA_NU;
+                              : (6 * VCA_NU * ES * W * W > VCA_STAGE_MAX) ? (VCA_GROUPS == 4 ? 1 : 2) : VCA_NU;
     // (VCA_GROUPS = 4 is an A/B variant only: 16 consumer warps at 112 registers, NU = 3,
     // 2 x 18 KB stages per group -- 3 % slower on config 3, profiles/r01d/ab_groups4.log)
     static constexpr int UNITS = 4 * NU;                   // units per strip (4 consumer warps)
@@ -237,7 +240,10 @@ struct Fam {
 #ifndef VCA_RING
 #define VCA_RING 55296  // ring bytes per consumer group: 3 x 18 KB (NU = 3), 2 x 24 KB (NU = 4)
 #endif
-    static constexpr int RING = VCA_RING;  // ring bytes per CTA (several CTAs per SM)
+#ifndef VCA_RING16
+#define VCA_RING16 VCA_RING  // ring of the n = 16 luma families (A/B of larger strips)
+#endif
+    static constexpr int RING = NY == 16 ? VCA_RING16 : VCA_RING;  // ring bytes per consumer group
     static constexpr int STAGES = (RING / STAGE) < 2 ? 2 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);
 #ifndef VCA_NO_HMMA10
