@@ -117,7 +117,9 @@ size_t vca_scratch_bytes(const vca_ctx *ctx, int max_frames);
  *   shard, R-7).  n_frames >= 1 + n_halo, else VCA_ERR_INVALID_ARG.
  * scratch / scratch_bytes: caller-owned device memory of at least
  *   vca_scratch_bytes(ctx, n_frames) bytes (VCA_ERR_SCRATCH otherwise),
- *   8-byte aligned; clobbered.
+ *   8-byte aligned; clobbered.  After the call (stream-ordered) it begins with
+ *   the per-block luma energies H_Y (A5, the inputs of h) as doubles
+ *   [n_frames][rows[0] * cols[0]] in raster block order -- the halo frame's too.
  * out_dev: device array of n_frames - n_halo records, written in POC order.
  *   Record i has poc = next_poc + i, where next_poc is the context's POC
  *   counter (0 after create; see vca_reset), advanced by n_frames - n_halo.

@@ -223,24 +223,33 @@ def test_profile_counters():
 @pytest.mark.parametrize("cfg", (2, 3, 4))
 def test_parity_full_size_all_frames(cfg):
     """Full BASELINE.json geometry and batch, analysed in one call (the launch configuration
-    bench.py times); every record against the oracle (chunks behind a halo frame for h), every
-    feature finite and non-negative, and the coefficient dump of the last frame."""
+    bench.py times); every record and every block's luma energy H_Y against the oracle (chunks
+    behind a halo frame for h), every feature finite and non-negative, and the coefficient dump
+    of the last frame."""
     c = synth.CONFIGS[cfg]
     F = c.n_frames            # the whole BASELINE.json batch in one call, as bench.py times it
     Y, U, V = synth.config_frames(cfg, device="cuda", n_frames=F)
     a = Analyzer(c.width, c.height, c.bit_depth, c.block_size, c.lowpass)
-    g = records_to_numpy(a.analyze(Y, U, V))
+    scratch = torch.empty(a.scratch_bytes(F) // 8 + 1, dtype=torch.float64, device="cuda")
+    g = records_to_numpy(a.analyze(Y, U, V, scratch=scratch))
+    CY = a.info["rows"][0] * a.info["cols"][0]
+    HY = scratch[:F * CY].view(F, CY).cpu().numpy()   # per-block luma H of every frame (vca.h)
     assert len(g) == F and np.array_equal(g["poc"], np.arange(F))
     for f in FEATS:            # properties of every frame: finite, non-negative
         assert np.all(np.isfinite(g[f])) and np.all(g[f] >= 0.0), f
-    # every frame against the oracle, in host-sized chunks (each behind a one-frame halo for h)
+    # every frame against the oracle, in host-sized chunks (each behind a one-frame halo for h),
+    # and every block's H_Y (a wrong coefficient moves H by >= w_min / (4096 n), far above
+    # the 1e-12 relative bar of two FP64 summation orders)
     step = 40
     for s in range(0, F, step):
         e = min(F, s + step)
         h0 = 1 if s > 0 else 0
         npl = synth.as_numpy_planes(Y[s - h0:e], U[s - h0:e], V[s - h0:e])
-        r = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=h0, first_poc=s)
+        r, rHY = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=h0, first_poc=s,
+                                want_HY=True)
         assert_records(g[s:e], r)
+        want = rHY[h0:]
+        assert np.all(np.abs(HY[s:e] - want) <= 1e-12 * np.maximum(want, 1e-300)), s
     Yc, Uc, Vc = (p[F - 1:F].cpu() for p in (Y, U, V))
     check_dump(a, Yc, Uc, Vc, c.bit_depth, c.block_size, c.lowpass, frame=0)
 
