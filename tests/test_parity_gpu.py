@@ -248,6 +248,10 @@ def test_parity_full_size_all_frames(cfg):
         r, rHY = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=h0, first_poc=s,
                                 want_HY=True)
         assert_records(g[s:e], r)
+        # and far inside it: the two sides differ only in FP64 summation order (measured
+        # <= 2e-14, tools/parity_margins.py), while one wrong chroma coefficient would move
+        # E_U or E_V by ~1e-10 relative -- invisible at 1e-6, caught here
+        assert_records(g[s:e], r, rtol=1e-12)
         want = rHY[h0:]
         assert np.all(np.abs(HY[s:e] - want) <= 1e-12 * np.maximum(want, 1e-300)), s
     Yc, Uc, Vc = (p[F - 1:F].cpu() for p in (Y, U, V))
