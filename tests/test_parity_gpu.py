@@ -249,7 +249,7 @@ def test_parity_full_size_all_frames(cfg):
                                 want_HY=True)
         assert_records(g[s:e], r)
         # and far inside it: the two sides differ only in FP64 summation order (measured
-        # <= 2e-14, tools/parity_margins.py), while one wrong chroma coefficient would move
+        # <= 2e-14, tests/test_parity_margins_gpu.py), while one wrong chroma coefficient would move
         # E_U or E_V by ~1e-10 relative -- invisible at 1e-6, caught here
         assert_records(g[s:e], r, rtol=1e-12)
         want = rHY[h0:]
