@@ -111,9 +111,17 @@ def test_parity_small(name, W, H, bd, w, lp):
 
 
 def test_parity_config1_cif_all_frames():
+    """Config 1 whole (16 CIF frames, one call): records at 1e-6 and 1e-12, every block's H_Y,
+    and every coefficient of every fifth frame."""
     Y, U, V = synth.config_frames(1)
-    g, r, a = run_both(Y, U, V, 8, 32, False)
+    a = Analyzer(352, 288, 8, 32, False)
+    scratch = torch.empty(a.scratch_bytes(16) // 8 + 1, dtype=torch.float64, device="cuda")
+    g = records_to_numpy(a.analyze(*planes_cuda(Y, U, V), scratch=scratch))
+    r, rHY = oracle.analyze(*synth.as_numpy_planes(Y, U, V), 8, 32, False, want_HY=True)
     assert_records(g, r)
+    assert_records(g, r, rtol=1e-12)
+    HY = scratch[:rHY.size].view(rHY.shape).cpu().numpy()
+    assert np.all(np.abs(HY - rHY) <= 1e-12 * np.maximum(rHY, 1e-300))
     for t in range(0, 16, 5):
         check_dump(a, Y, U, V, 8, 32, False, frame=t)
 
