@@ -4,7 +4,7 @@
 //
 // One work item = one block row r of one frame f; a unit = the co-located Y block
 // (w x w) and U, V blocks (w/2 x w/2) of (f, r, c); a strip = 4 * NU consecutive units.
-// One persistent CTA per SM, warp-specialised (kGroups = 3):
+// One persistent CTA per SM, warp-specialised (3 consumer groups; 4 for the n = 8 families):
 //
 //  * warpgroup 0: producers (setmaxnreg.dec).  Warp g's elected lane feeds consumer
 //    group g: per strip one 3-D tensor-map load per plane box (swizzled, zero-filled out
@@ -201,6 +201,14 @@ struct Fam {
     static constexpr int ES = BD == 8 ? 1 : 2;
     static constexpr int NY = LP ? W / 2 : W;
     static constexpr int NC = LP ? WC / 2 : WC;
+#ifndef VCA_GROUPS8
+#define VCA_GROUPS8 4  // consumer groups of the n = 8 families (A/B: 4 groups of 112 registers, NU8 = 4:
+                       // 1080p lp16 +3 %, 1080p w8 +7 %, 720p lp16 +20 %, 720p w8 +-0 vs 3 groups, NU8 = 8)
+#endif
+    // consumer groups per CTA (0: the legacy one-producer-warp layout), threads per CTA
+    static constexpr int G = NY == 8 ? VCA_GROUPS8 : VCA_GROUPS;
+    static constexpr int GV = G ? G : 1;
+    static constexpr int THREADS = G ? 128 * (1 + G) : 160;
 #ifndef VCA_NU
 #define VCA_NU (VCA_GROUPS == 3 ? 4 : 2)
 #endif
@@ -208,7 +216,9 @@ struct Fam {
 #define VCA_STAGE_MAX 24576  // largest n = 16 luma stage (6 NU ES W^2 bytes) before NU falls back to 2
 #endif
 #ifndef VCA_NU8
-#define VCA_NU8 8  // units per warp per strip, n = 8 families (multiple of 4; A/B: 8 vs 4 +6.5 % 1080p lp16, +17 % 720p w8)
+// units per warp per strip, n = 8 families (multiple of 4; with 3 groups, A/B: 8 vs 4 +6.5 %
+// 1080p lp16, +17 % 720p w8; 4 groups fit only 4 in shared memory)
+#define VCA_NU8 (VCA_GROUPS8 == 4 ? 4 : 8)
 #endif
 #ifndef VCA_NU32
 #define VCA_NU32 2  // units per consumer warp per strip for the n = 32 luma path (A/B: 1 -> 2 +3 %)
@@ -243,7 +253,10 @@ struct Fam {
 #ifndef VCA_RING16
 #define VCA_RING16 VCA_RING  // ring of the n = 16 luma families (A/B of larger strips)
 #endif
-    static constexpr int RING = NY == 16 ? VCA_RING16 : VCA_RING;  // ring bytes per consumer group
+#ifndef VCA_RING8
+#define VCA_RING8 (VCA_GROUPS8 == 4 ? 36864 : VCA_RING)  // ring of the n = 8 families
+#endif
+    static constexpr int RING = NY == 16 ? VCA_RING16 : NY == 8 ? VCA_RING8 : VCA_RING;  // ring bytes per consumer group
     static constexpr int STAGES = (RING / STAGE) < 2 ? 2 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);
 #ifndef VCA_NO_HMMA10
@@ -1300,36 +1313,35 @@ struct Regs {
 #ifdef VCA_PREG
     static constexpr int P = VCA_PREG;
 #else
-    static constexpr int P = VCA_GROUPS == 3 ? 24 : 40;
+    static constexpr int P = (F::G == 3 || F::G == 4) ? 24 : 40;
 #endif
 #ifdef VCA_CREG
     static constexpr int C = VCA_CREG;
 #else
-    static constexpr int C = VCA_GROUPS == 2 ? 232 : VCA_GROUPS == 3 ? 160 : 104;
+    // G = 4: the launch pool is 640 threads x 96 registers, so 128 x 24 + 512 x C <= 61440
+    static constexpr int C = F::G == 2 ? 232 : F::G == 3 ? 160 : 112;
 #endif
 };
-constexpr int kGroups = VCA_GROUPS;
-constexpr int kGv = kGroups ? kGroups : 1;  // consumer groups per CTA
-constexpr int kFusedThreads = kGroups ? 128 * (1 + kGroups) : 160;
 constexpr int kConsumers = 4;
 
 template <class F>
 struct Lay {  // shared-memory layout (offsets from the 1024-aligned base)
     static constexpr int GRP = (F::STAGES * F::STAGE + 2 * F::STAGES * 8 + 1023) / 1024 * 1024;  // ring + bars
-    static constexpr int WTAB_OFF = kGv * GRP;
+    static constexpr int WTAB_OFF = F::GV * GRP;
     static constexpr int STASH_OFF = WTAB_OFF + (F::WTAB ? 32 * 32 * 8 : 0);
-    static constexpr int WSM_OFF = STASH_OFF + 4 * kGv * F::STASH;
-    static constexpr int SMEM = 1024 + WSM_OFF + kGv * 10 * 32 * 8;
+    static constexpr int WSM_OFF = STASH_OFF + 4 * F::GV * F::STASH;
+    static constexpr int SMEM = 1024 + WSM_OFF + F::GV * 10 * 32 * 8;
     static_assert(SMEM <= 232448, "dynamic shared memory over the 227 KB per-CTA limit");
 };
 
 template <int W_, int BD_, int LP_, bool DUMP>
-__global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>::MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
+__global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>::G ? 1 : Fam<W_, BD_, LP_>::MINB) fused_kernel(const __grid_constant__ CUtensorMap tmY,
                                                     const __grid_constant__ CUtensorMap tmU,
                                                     const __grid_constant__ CUtensorMap tmV, const FusedArgs a)
 {
     using F = Fam<W_, BD_, LP_>;
     constexpr int NY = F::NY, NC = F::NC, W = F::W, WC = F::WC, NU = F::NU;
+    constexpr int kGroups = F::G, kGv = F::GV;
     uint8_t *smem_raw = vca_dyn_smem;
     using Y = Lay<F>;
     uint8_t *smem0p = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1375,9 +1387,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
 
     if (kGroups ? warp < 4 : warp == 0) {
         // ---------------- TMA producer (A1)
-#if VCA_GROUPS
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Regs<F>::P));
-#endif
+        if constexpr (kGroups != 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Regs<F>::P));
         if (lane == 0 && warp < kGv) {
             uint64_t policy;
             asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
@@ -1427,9 +1437,7 @@ __global__ void __launch_bounds__(kFusedThreads, kGroups ? 1 : Fam<W_, BD_, LP_>
     }
 
     // ---------------- consumers
-#if VCA_GROUPS
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Regs<F>::C));
-#endif
+    if constexpr (kGroups != 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Regs<F>::C));
     const int u = kGroups ? (warp & 3) : warp - 1;
     const int g = lane >> 2, t = lane & 3;
     const uint32_t hst = smem_off(stash) + (grp * 4 + u) * F::STASH;  // [32][9] doubles
@@ -1770,14 +1778,14 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     const bool dump = dp.coeffs[0] != nullptr;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
     int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFusedThreads, Lay<F>::SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F::THREADS, Lay<F>::SMEM) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     const int64_t items = (int64_t)n_frames * a.rows;
     if (items > 0x7fffffff) return -2;
     int64_t grid = (int64_t)sm_count * per_sm;
     if (grid > items) grid = items;
-    kern<<<(unsigned)grid, kFusedThreads, Lay<F>::SMEM, st>>>(mY, mU, mV, a);
+    kern<<<(unsigned)grid, F::THREADS, Lay<F>::SMEM, st>>>(mY, mU, mV, a);
     return 0;
 }
 
