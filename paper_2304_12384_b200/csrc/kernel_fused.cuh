@@ -206,7 +206,10 @@ struct Fam {
                        // 1080p lp16 +3 %, 1080p w8 +7 %, 720p lp16 +20 %, 720p w8 +-0 vs 3 groups, NU8 = 8)
 #endif
     // consumer groups per CTA (0: the legacy one-producer-warp layout), threads per CTA
-    static constexpr int G = NY == 8 ? VCA_GROUPS8 : VCA_GROUPS;
+#ifndef VCA_GROUPS32
+#define VCA_GROUPS32 VCA_GROUPS  // consumer groups of the n = 32 families (A/B)
+#endif
+    static constexpr int G = NY == 8 ? VCA_GROUPS8 : NY == 32 ? VCA_GROUPS32 : VCA_GROUPS;
     static constexpr int GV = G ? G : 1;
     static constexpr int THREADS = G ? 128 * (1 + G) : 160;
 #ifndef VCA_NU
@@ -256,7 +259,10 @@ struct Fam {
 #ifndef VCA_RING8
 #define VCA_RING8 (VCA_GROUPS8 == 4 ? 36864 : VCA_RING)  // ring of the n = 8 families
 #endif
-    static constexpr int RING = NY == 16 ? VCA_RING16 : NY == 8 ? VCA_RING8 : VCA_RING;  // ring bytes per consumer group
+#ifndef VCA_RING32
+#define VCA_RING32 VCA_RING  // ring of the n = 32 families (A/B)
+#endif
+    static constexpr int RING = NY == 16 ? VCA_RING16 : NY == 8 ? VCA_RING8 : NY == 32 ? VCA_RING32 : VCA_RING;
     static constexpr int STAGES = (RING / STAGE) < 2 ? 2 : (RING / STAGE > 16 ? 16 : RING / STAGE);
     static constexpr bool WTAB = (NY == 32);
 #ifndef VCA_NO_HMMA10
