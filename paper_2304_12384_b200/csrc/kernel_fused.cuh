@@ -212,6 +212,7 @@ struct Fam {
     static constexpr int G = NY == 8 ? VCA_GROUPS8 : NY == 32 ? VCA_GROUPS32 : VCA_GROUPS;
     static constexpr int GV = G ? G : 1;
     static constexpr int THREADS = G ? 128 * (1 + G) : 160;
+    static_assert(G >= 0 && G <= 4, "one producer warp per consumer group, all in warpgroup 0");
 #ifndef VCA_NU
 #define VCA_NU (VCA_GROUPS == 3 ? 4 : 2)
 #endif
@@ -221,7 +222,7 @@ struct Fam {
 #ifndef VCA_NU8
 // units per warp per strip, n = 8 families (multiple of 4; with 3 groups, A/B: 8 vs 4 +6.5 %
 // 1080p lp16, +17 % 720p w8; 4 groups fit only 4 in shared memory)
-#define VCA_NU8 (VCA_GROUPS8 == 4 ? 4 : 8)
+#define VCA_NU8 (VCA_GROUPS8 >= 4 ? 4 : 8)
 #endif
 #ifndef VCA_NU32
 #define VCA_NU32 2  // units per consumer warp per strip for the n = 32 luma path (A/B: 1 -> 2 +3 %)
@@ -1319,7 +1320,7 @@ struct Regs {
 #ifdef VCA_PREG
     static constexpr int P = VCA_PREG;
 #else
-    static constexpr int P = (F::G == 3 || F::G == 4) ? 24 : 40;
+    static constexpr int P = F::G >= 3 ? 24 : 40;
 #endif
 #ifdef VCA_CREG
     static constexpr int C = VCA_CREG;
