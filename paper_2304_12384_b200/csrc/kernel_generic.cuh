@@ -121,93 +121,148 @@ generic_block_kernel(Planes3 planes, int n_frames, int lowpass, const int8_t *__
 }
 
 // Thread-per-block kernel for the n = 4 family (w = 4 full; its chroma grid differs from
-// the luma grid, so the fused kernel's units do not apply).  One thread computes one 4 x 4
-// block of one plane of one frame; consecutive threads take consecutive blocks of a block
-// row, so a warp's row loads are 128 (8-bit) or 256 (10-bit) contiguous bytes.  Same
-// arithmetic as generic_block_kernel: exact int32 C = T X T^T (|C| <= 256^2 * 1023 < 2^27),
-// FP64 H and L, one (H, L) partial per block for the fixed-order finalize.
-template <int BD>
+// the luma grid, so the fused kernel's units do not apply).  One warp takes a chunk of 32
+// consecutive blocks of one plane of one frame (chunks never cross planes), one lane per
+// 4 x 4 block, so a warp's row loads are 128 (8-bit) or 256 (10-bit) contiguous bytes; the
+// (frame, plane, chunk) tasks are flattened so every warp stays busy across frames.
+// A4 exact: the horizontal pass Z[y][j] = sum_x X[y][x] T[j][x] is a byte dot product of the
+// packed row with the packed basis row (one IDP.4A, u8 x s8; 10-bit: two IDP.2A, u16 x s8),
+// the vertical pass C[i][j] = sum_y T[i][y] Z[y][j] is int32 IMAD (|C| <= 256^2 * 1023 < 2^27);
+// FP64 H and L.  The chunk's 32 (H, L) pairs are reduced in a fixed xor order and written as
+// ONE partial (the finalize then adds ceil(C_p / 32) partials per plane in index order), so
+// the per-block write traffic is only H_Y (needed for h).  DUMP: the test-only coefficient dump.
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c)
+{
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_us(uint32_t lo, uint32_t hi, uint32_t b)
+{
+    int d;
+    asm("dp2a.lo.u32.s32 %0, %1, %2, 0;\n\tdp2a.hi.u32.s32 %0, %3, %2, %0;" : "=&r"(d) : "r"(lo), "r"(b), "r"(hi));
+    return d;
+}
+
+#ifndef VCA_W4_B
+#define VCA_W4_B 1  // 4 x 4 blocks per lane per chunk (chunk = 32 VCA_W4_B blocks; A/B: 2 and 4 -30 %)
+#endif
+
+template <int BD, bool DUMP>
 __global__ void __launch_bounds__(256)
 small_block_kernel(Planes3 planes, int n_frames, const int8_t *__restrict__ T_all, const double *__restrict__ W_all,
                    Scratch s, DumpPtrs dump)
 {
     int T[4][4];
+    uint32_t Tp[4];  // basis rows packed as s8 x 4
     double Wt[4][4];
     const int8_t *T4 = T_all + table_offset(4);
     const double *W4 = W_all + table_offset(4);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i) {
+        Tp[i] = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             T[i][j] = (int)__ldg(T4 + i * 4 + j);
+            Tp[i] |= (uint32_t)(T[i][j] & 255) << (8 * j);
             Wt[i][j] = __ldg(W4 + i * 4 + j);
         }
-    // 32-bit block indices within a frame (C_Y + C_U + C_V < 2^31, checked on the host),
-    // frames in an outer loop: no 64-bit divisions on the per-block path
+    }
+    // 32-bit block indices within a frame (C_Y + C_U + C_V < 2^31, checked on the host)
     const int C0 = (int)planes.p[0].count, C1 = (int)planes.p[1].count, C2 = (int)planes.p[2].count;
-    const int Ctot = C0 + C1 + C2;
-    const int stride = gridDim.x * blockDim.x;
-    for (int f = 0; f < n_frames; ++f)
-    for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < Ctot; kk += stride) {
-        int k = kk, p = 0;
-        if (k >= C0) { k -= C0; p = 1; if (k >= C1) { k -= C1; p = 2; } }
+    constexpr int CHB = 32 * VCA_W4_B;  // blocks per chunk
+    const int CH0 = (C0 + CHB - 1) / CHB, CH1 = (C1 + CHB - 1) / CHB, CH2 = (C2 + CHB - 1) / CHB;
+    const int CHtot = CH0 + CH1 + CH2;
+    const int64_t tasks = (int64_t)n_frames * CHtot;
+    const int lane = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); task < tasks;
+         task += wstride) {
+        const int f = (int)(task / CHtot);
+        int ch = (int)(task - (int64_t)f * CHtot), p = 0;
+        if (ch >= CH0) { ch -= CH0; p = 1; if (ch >= CH1) { ch -= CH1; p = 2; } }
         // plane fields by selects (a dynamically indexed parameter array would go to local memory)
         PlaneDesc P = planes.p[0];
         if (p == 1) P = planes.p[1];
         if (p == 2) P = planes.p[2];
-        const int r = k / P.cols, c = k - r * P.cols;
-        const uint8_t *frame = P.base + (int64_t)f * P.fstride;
-        // A2: gather (edge replication; 10-bit clamp)
-        int X[4][4];
-        const bool whole = c * 4 + 3 < P.width;
+        const int Cp = p == 0 ? C0 : p == 1 ? C1 : C2;
+        double h = 0.0, L = 0.0;
 #pragma unroll
-        for (int y = 0; y < 4; ++y) {
-            const int yy = min(r * 4 + y, P.height - 1);
-            const uint8_t *row = frame + (int64_t)yy * P.pitch;
-            if (whole && BD == 8) {
-                const uint32_t v = *reinterpret_cast<const uint32_t *>(row + 4 * c);
+        for (int b = 0; b < VCA_W4_B; ++b) {
+            const int k = (ch * VCA_W4_B + b) * 32 + lane;
+            if (k < Cp) {
+                double hb = 0.0;
+                const int r = k / P.cols, c = k - r * P.cols;
+                const uint8_t *frame = P.base + (int64_t)f * P.fstride;
+                // A2 gather (edge replication; 10-bit clamp) + A4 horizontal pass
+                int Z[4][4];  // Z[y][j]
+                const bool whole = c * 4 + 3 < P.width;
 #pragma unroll
-                for (int x = 0; x < 4; ++x) X[y][x] = (int)((v >> (8 * x)) & 255u);
-            } else if (whole) {
-                const uint2 v = *reinterpret_cast<const uint2 *>(row + 8 * c);
-                X[y][0] = min((int)(v.x & 0xFFFFu), 1023);
-                X[y][1] = min((int)(v.x >> 16), 1023);
-                X[y][2] = min((int)(v.y & 0xFFFFu), 1023);
-                X[y][3] = min((int)(v.y >> 16), 1023);
-            } else {
+                for (int y = 0; y < 4; ++y) {
+                    const int yy = min(r * 4 + y, P.height - 1);
+                    const uint8_t *row = frame + (int64_t)yy * P.pitch;
+                    if (BD == 8) {
+                        uint32_t v;
+                        if (whole) {
+                            v = *reinterpret_cast<const uint32_t *>(row + 4 * c);
+                        } else {
+                            v = 0;
 #pragma unroll
-                for (int x = 0; x < 4; ++x) X[y][x] = load_sample<BD>(frame, P, c * 4 + x, yy);
+                            for (int x = 0; x < 4; ++x) v |= (uint32_t)load_sample<8>(frame, P, c * 4 + x, yy) << (8 * x);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) Z[y][j] = dp4a_us(v, Tp[j], 0);
+                    } else {
+                        uint32_t lo, hi;
+                        if (whole) {
+                            const uint2 v = *reinterpret_cast<const uint2 *>(row + 8 * c);
+                            lo = __vminu2(v.x, 0x03FF03FFu);
+                            hi = __vminu2(v.y, 0x03FF03FFu);
+                        } else {
+                            lo = (uint32_t)load_sample<10>(frame, P, c * 4, yy) |
+                                 ((uint32_t)load_sample<10>(frame, P, c * 4 + 1, yy) << 16);
+                            hi = (uint32_t)load_sample<10>(frame, P, c * 4 + 2, yy) |
+                                 ((uint32_t)load_sample<10>(frame, P, c * 4 + 3, yy) << 16);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) Z[y][j] = dp2a_us(lo, hi, Tp[j]);
+                    }
+                }
+                // A4 vertical pass, A5 (row-major, DC excluded)
+                int c00 = 0;
+                int32_t *dco = nullptr;
+                if (DUMP) dco = p == 0 ? dump.coeffs[0] : p == 1 ? dump.coeffs[1] : dump.coeffs[2];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int cij = T[i][0] * Z[0][j] + T[i][1] * Z[1][j] + T[i][2] * Z[2][j] + T[i][3] * Z[3][j];
+                        if (i == 0 && j == 0) c00 = cij;
+                        else hb = fma(Wt[i][j], (double)(cij < 0 ? -cij : cij), hb);
+                        if (DUMP) dco[(int64_t)k * 16 + i * 4 + j] = cij;
+                    }
+                const int64_t sumx = c00 >> 12;         // C_00 = 4096 * sum(X) exactly
+                const double Lb = sqrt((double)sumx / 4.0);  // A6
+                h += hb;  // per lane: block b = 0, 1, ... in order
+                L += Lb;
+                if (p == 0) s.HY[(int64_t)f * C0 + k] = hb;
+                if (DUMP) {  // debug dump (all three planes are dumped together)
+                    (p == 0 ? dump.sumx[0] : p == 1 ? dump.sumx[1] : dump.sumx[2])[k] = sumx;
+                    (p == 0 ? dump.H[0] : p == 1 ? dump.H[1] : dump.H[2])[k] = hb;
+                    (p == 0 ? dump.L[0] : p == 1 ? dump.L[1] : dump.L[2])[k] = Lb;
+                }
             }
         }
-        // A4: Z[i][x] = sum_y T[i][y] X[y][x]; C[i][j] = sum_x Z[i][x] T[j][x]  (exact int32)
-        int Z[4][4];
+        // A7 input: the chunk's fixed-order partial (xor tree over the 32 blocks)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-                Z[i][x] = T[i][0] * X[0][x] + T[i][1] * X[1][x] + T[i][2] * X[2][x] + T[i][3] * X[3][x];
-        double h = 0.0;
-        int c00 = 0;
-        int32_t *const dco = p == 0 ? dump.coeffs[0] : p == 1 ? dump.coeffs[1] : dump.coeffs[2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int cij = Z[i][0] * T[j][0] + Z[i][1] * T[j][1] + Z[i][2] * T[j][2] + Z[i][3] * T[j][3];
-                if (i == 0 && j == 0) c00 = cij;
-                else h = fma(Wt[i][j], (double)(cij < 0 ? -cij : cij), h);  // A5, row-major, DC excluded
-                if (dco) dco[(int64_t)k * 16 + i * 4 + j] = cij;
-            }
-        const int64_t sumx = c00 >> 12;               // C_00 = 4096 * sum(X) exactly
-        const double L = sqrt((double)sumx / 4.0);    // A6
-        double *pp = s.partial + (((int64_t)f * 3 + p) * s.P + k) * 2;
-        pp[0] = h;
-        pp[1] = L;
-        if (p == 0) s.HY[(int64_t)f * C0 + k] = h;
-        if (dco) {  // debug dump (all three planes are dumped together)
-            (p == 0 ? dump.sumx[0] : p == 1 ? dump.sumx[1] : dump.sumx[2])[k] = sumx;
-            (p == 0 ? dump.H[0] : p == 1 ? dump.H[1] : dump.H[2])[k] = h;
-            (p == 0 ? dump.L[0] : p == 1 ? dump.L[1] : dump.L[2])[k] = L;
+        for (int o = 16; o > 0; o >>= 1) {
+            h += __shfl_xor_sync(0xffffffffu, h, o);
+            L += __shfl_xor_sync(0xffffffffu, L, o);
+        }
+        if (lane == 0) {
+            double *pp = s.partial + (((int64_t)f * 3 + p) * s.P + ch) * 2;
+            pp[0] = h;
+            pp[1] = L;
         }
     }
 }

@@ -70,6 +70,18 @@ int fail_cuda(vca_ctx *ctx, cudaError_t e)
     return VCA_OK;
 }
 
+// the w = 4 family runs small_block_kernel (thread per block) unless the warp-generic
+// kernel is forced for every family
+inline bool small_path(const vca_ctx *c)
+{
+#ifdef VCA_FORCE_GENERIC
+    (void)c;
+    return false;
+#else
+    return c->path == VCA_PATH_WARP_GENERIC && c->geo[0].n == 4 && c->geo[1].n == 4 && !c->lowpass;
+#endif
+}
+
 #define VCA_CK(ctx, call)                                    \
     do {                                                     \
         cudaError_t e_ = (call);                             \
@@ -192,16 +204,25 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         const int64_t cap = (int64_t)ctx->sm_count * 16;
         if (blocks > cap) blocks = cap;
 #ifndef VCA_FORCE_GENERIC
-        if (ctx->geo[0].n == 4 && ctx->geo[1].n == 4 && !ctx->lowpass) {  // w = 4: thread per block
+        if (small_path(ctx)) {  // w = 4: thread per block, warp per 32-block chunk
             const int64_t per_frame = ctx->geo[0].count + ctx->geo[1].count + ctx->geo[2].count;
             if (per_frame > 0x7fffffff) return VCA_ERR_INVALID_ARG;
-            int64_t tb = (per_frame + 255) / 256;
+            const int64_t chunks = (int64_t)n_frames * (ctx->Pp[0] + ctx->Pp[1] + ctx->Pp[2]);
+            int64_t tb = (chunks + 7) / 8;  // 8 warps per 256-thread CTA
             const int64_t tcap = (int64_t)ctx->sm_count * 8;
             if (tb > tcap) tb = tcap;
-            if (ctx->bd == 8)
-                small_block_kernel<8><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
-            else
-                small_block_kernel<10><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+            const bool dmp = dp.coeffs[0] != nullptr;
+            if (ctx->bd == 8) {
+                if (dmp)
+                    small_block_kernel<8, true><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+                else
+                    small_block_kernel<8, false><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+            } else {
+                if (dmp)
+                    small_block_kernel<10, true><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+                else
+                    small_block_kernel<10, false><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
+            }
         } else
 #endif
         if (ctx->bd == 8)
@@ -301,6 +322,9 @@ int vca_create(int width, int height, int bit_depth, int chroma_format, int bloc
     if (c->path == VCA_PATH_FUSED_MMA) {
         const int pr = fused_partials_per_row();
         for (int p = 0; p < 3; ++p) c->Pp[p] = c->geo[p].rows * pr;
+    } else if (small_path(c)) {
+        for (int p = 0; p < 3; ++p)  // one partial per chunk of 32 VCA_W4_B blocks
+            c->Pp[p] = (int)((c->geo[p].count + 32 * VCA_W4_B - 1) / (32 * VCA_W4_B));
     } else {
         for (int p = 0; p < 3; ++p) c->Pp[p] = (int)c->geo[p].count;
     }
