@@ -20,6 +20,7 @@ struct FinalizeArgs {
     int64_t count[3];
     int n[3];
     const double *prevHY;  // H_Y of the frame before frame 0 (carried), or nullptr
+    double *saveHY;        // receives the last frame's H_Y (the next call's prevHY; another buffer)
     int64_t first_poc;
     vca_features *out;
 };
@@ -66,6 +67,9 @@ __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs
     const double *prev = f > 0 ? cur - a.count[0] : a.prevHY;
     if (prev) {
         for (int64_t k = tid; k < a.count[0]; k += kFinalizeThreads) v[6] += fabs(cur[k] - prev[k]);
+    }
+    if (f == a.n_frames - 1) {  // carry H_Y to the next call (R-7), no separate copy on the stream
+        for (int64_t k = tid; k < a.count[0]; k += kFinalizeThreads) a.saveHY[k] = cur[k];
     }
     block_reduce<7>(v, sm);
     if (tid == 0 && f >= a.n_halo) {

@@ -31,6 +31,8 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <atomic>
+
 #include "kernel_generic.cuh"
 #include "vca_common.cuh"
 
@@ -1784,10 +1786,16 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     a.dump = dp;
     const bool dump = dp.coeffs[0] != nullptr;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
-    int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F::THREADS, Lay<F>::SMEM) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
+    // CTAs per SM: a property of the kernel and the device, queried once per instantiation
+    // (the query costs microseconds of host time on every call otherwise)
+    static std::atomic<int> cached[2] = {0, 0};
+    int per_sm = cached[dump].load(std::memory_order_relaxed);
+    if (per_sm < 1) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, F::THREADS, Lay<F>::SMEM) != cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        cached[dump].store(per_sm, std::memory_order_relaxed);
+    }
     const int64_t items = (int64_t)n_frames * a.rows;
     if (items > 0x7fffffff) return -2;
     int64_t grid = (int64_t)sm_count * per_sm;

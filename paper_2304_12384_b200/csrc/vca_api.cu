@@ -38,7 +38,8 @@ struct vca_ctx {
     int device = 0, sm_count = 148;
     int8_t *d_T = nullptr;     // basis tables, all sizes
     double *d_W = nullptr;     // scaled weight tables, all sizes
-    double *d_prevHY = nullptr;
+    double *d_prevHY = nullptr;  // two buffers of C_Y doubles: [cur_prev] holds the carried H_Y
+    int cur_prev = 0;
     bool prev_valid = false;
     int64_t next_poc = 0;
     bool poisoned = false;
@@ -245,7 +246,9 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         fa.count[p] = ctx->geo[p].count;
         fa.n[p] = ctx->geo[p].n;
     }
-    fa.prevHY = (n_halo == 0 && ctx->prev_valid) ? ctx->d_prevHY : nullptr;
+    const size_t CY = (size_t)ctx->geo[0].count;
+    fa.prevHY = (n_halo == 0 && ctx->prev_valid) ? ctx->d_prevHY + ctx->cur_prev * CY : nullptr;
+    fa.saveHY = ctx->d_prevHY + (1 - ctx->cur_prev) * CY;
     fa.first_poc = ctx->next_poc;
     fa.out = out;
     finalize_kernel<<<n_frames, kFinalizeThreads, 0, st>>>(fa);
@@ -255,9 +258,8 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         VCA_CK(ctx, cudaEventRecord(ev.e[2], st));
         ctx->pending.push_back(ev);
     }
-    // carry H_Y of the last frame for the next call (R-7)
-    VCA_CK(ctx, cudaMemcpyAsync(ctx->d_prevHY, s.HY + (size_t)(n_frames - 1) * (size_t)ctx->geo[0].count,
-                                sizeof(double) * (size_t)ctx->geo[0].count, cudaMemcpyDeviceToDevice, st));
+    // the finalize kernel wrote the last frame's H_Y into the other buffer (R-7)
+    ctx->cur_prev = 1 - ctx->cur_prev;
     ctx->prev_valid = true;
     ctx->next_poc += n_frames - n_halo;
     return VCA_OK;
@@ -340,7 +342,7 @@ int vca_create(int width, int height, int bit_depth, int chroma_format, int bloc
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_T, sizeof(hT));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_W, sizeof(hW));
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_prevHY, sizeof(double) * (size_t)c->geo[0].count);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_prevHY, 2 * sizeof(double) * (size_t)c->geo[0].count);
     if (e == cudaSuccess) e = cudaMemcpy(c->d_T, hT, sizeof(hT), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(c->d_W, hW, sizeof(hW), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && c->path == VCA_PATH_FUSED_MMA) e = fused_prepare(c->bd, c->lowpass, w);
