@@ -1,6 +1,7 @@
-// kernel_fused.cuh -- the fused hot-path kernel (A1-A7) for the block
-// configurations of BASELINE.json: luma block w in {16, 32}, chroma block
-// w/2 on the same block grid, 8- or 10-bit, full or low-pass.
+// kernel_fused.cuh -- the fused hot-path kernel (A1-A7) for every block configuration
+// whose chroma grid equals the luma grid: luma block w in {8, 16, 32} (n = 32, 16, 8
+// families; low-pass needs w >= 16), chroma block w/2, 8- or 10-bit.  w = 4 (chroma grid
+// half the luma grid) runs small_block_kernel in kernel_generic.cuh.
 //
 // One work item = one block row r of one frame f; a unit = the co-located Y block
 // (w x w) and U, V blocks (w/2 x w/2) of (f, r, c); a strip = 4 * NU consecutive units.
@@ -9,7 +10,7 @@
 //  * warpgroup 0: producers (setmaxnreg.dec).  Warp g's elected lane feeds consumer
 //    group g: per strip one 3-D tensor-map load per plane box (swizzled, zero-filled out
 //    of bounds) into the group's ring of smem stages, full/empty mbarriers (A1);
-//  * warpgroups 1..3: consumer groups of 4 warps (setmaxnreg.inc), each walking its own
+//  * warpgroups 1..G: consumer groups of 4 warps (setmaxnreg.inc), each walking its own
 //    item sequence; warp u owns units u + 4n (n < NU) of every strip.  A consumer reads
 //    its units from smem with clamped row/column indices (edge replication, A2),
 //    low-pass-downsamples in registers with (s+2)>>2 (A3, R-5), and runs the exact
