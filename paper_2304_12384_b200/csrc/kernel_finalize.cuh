@@ -68,8 +68,11 @@ __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs
     if (prev) {
         for (int64_t k = tid; k < a.count[0]; k += kFinalizeThreads) v[6] += fabs(cur[k] - prev[k]);
     }
-    if (f == a.n_frames - 1) {  // carry H_Y to the next call (R-7), no separate copy on the stream
-        for (int64_t k = tid; k < a.count[0]; k += kFinalizeThreads) a.saveHY[k] = cur[k];
+    {  // carry the last frame's H_Y to the next call (R-7): every CTA copies a slice
+        const double *last = a.s.HY + (int64_t)(a.n_frames - 1) * a.count[0];
+        const int64_t per = (a.count[0] + a.n_frames - 1) / a.n_frames;
+        const int64_t k0 = (int64_t)f * per, k1 = min(a.count[0], k0 + per);
+        for (int64_t k = k0 + tid; k < k1; k += kFinalizeThreads) a.saveHY[k] = last[k];
     }
     block_reduce<7>(v, sm);
     if (tid == 0 && f >= a.n_halo) {
