@@ -1535,7 +1535,17 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
         for (int e = 0; e < ChromaAcc<F>::NP; ++e) ca.u[e] = ca.v[e] = 0u;
         double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // identical in all lanes
         double *HYrow = a.s.HY + (int64_t)f * CY + (int64_t)r * cols;
-        for (int s = 0; s < strips; ++s) {
+        // strips in chroma-flush windows of SPC: the flush runs once after each window (as its
+        // own block, not if-converted into predicated instructions issued on every strip:
+        // config 3 +1 %, config 4 +3.5 %, w = 16 full +7 %).  The n = 8 families keep the
+        // in-loop flush (the windowed loop measured -3 % there).
+        constexpr int SPC = ChromaAcc<F>::FC / NU;  // strips per chroma flush (<= FC units)
+        static_assert(SPC >= 1, "chroma flush period");
+        constexpr bool WIN = NY != 8;
+        constexpr int SPCW = WIN ? SPC : (1 << 30);
+        for (int s0 = 0; s0 < strips; s0 += SPCW) {
+        const int s1 = min(strips, s0 + SPCW);
+        for (int s = s0; s < s1; ++s) {
             mbar_wait(full0 + 8 * st, phase);
             // this warp's units of strip s: c_n = s*UNITS + u + 4n, n < NU, in ascending order;
             // unit m = s*NU + n of the item goes to stash slot m & 31
@@ -1635,10 +1645,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                 st = 0;
                 phase ^= 1;
             }
-            constexpr int SPC = ChromaAcc<F>::FC / NU;  // strips per chroma flush (<= FC units)
-            static_assert(SPC >= 1, "chroma flush period");
-            if (ChromaAcc<F>::ON && ((s % SPC) == SPC - 1 || s == strips - 1)) {
-                // chroma flush: weight the exact per-position sums once (fixed position order)
+            if (!WIN && ChromaAcc<F>::ON && ((s % SPC) == SPC - 1 || s == strips - 1)) {
 #pragma unroll
                 for (int e = 0; e < ChromaAcc<F>::NP; ++e) {
                     const double wce = NY == 8 ? U.w4[e] : U.wc[e];
@@ -1681,6 +1688,17 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                 sLV += LVl;
                 __syncwarp();
             }
+        }
+        if (WIN && ChromaAcc<F>::ON) {
+            // chroma flush: weight the exact per-position sums once (fixed position order)
+#pragma unroll
+            for (int e = 0; e < ChromaAcc<F>::NP; ++e) {
+                const double wce = NY == 8 ? U.w4[e] : U.wc[e];
+                hu = fma(wce, __uint2double_rn(ca.u[e]), hu);
+                hv = fma(wce, __uint2double_rn(ca.v[e]), hv);
+                ca.u[e] = ca.v[e] = 0u;
+            }
+        }
         }
         // ---- item end: fixed-order partials of this warp's units (A7 inputs)
 #pragma unroll
