@@ -148,8 +148,11 @@ __device__ __forceinline__ int dp2a_us(uint32_t lo, uint32_t hi, uint32_t b)
 #define VCA_W4_B 1  // 4 x 4 blocks per lane per chunk (chunk = 32 VCA_W4_B blocks; A/B: 2 and 4 -30 %)
 #endif
 
+#ifndef VCA_W4_MINB
+#define VCA_W4_MINB 8  // 8 CTAs x 256 threads per SM: 32 registers (A/B: 1080p 192k -> 214k fps vs the default budget)
+#endif
 template <int BD, bool DUMP>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, VCA_W4_MINB)
 small_block_kernel(Planes3 planes, int n_frames, const int8_t *__restrict__ T_all, const double *__restrict__ W_all,
                    Scratch s, DumpPtrs dump)
 {
