@@ -4,11 +4,13 @@
 Metric (BASELINE.json): UHD 8-bit 4:2:0 frames/sec for the 7 DCT features,
 at 1/2/4/8 GPUs, plus % of roofline.
 
-* N = 1: config 3 -- 600 UHD 8-bit frames, block 32, low-pass (seed 2).
-* N > 1 (torchrun, one rank per GPU, NCCL): config 5's construction, weak
-  scaling -- rank r analyses segment r (600 frames of G(10 + r)) with a
-  one-frame halo (the last frame of segment r - 1) and the per-frame records
-  are gathered to rank 0 over NCCL; at N = 8 this is config 5 exactly.
+* N = 1: config 3 -- 600 UHD 8-bit frames, block 32, low-pass (seed 2); plus
+  `config5_1gpu_4800`: config 5's 4800 frames on this one GPU (the strong-scaling
+  baseline fps_1 of BASELINE.json's efficiency target).
+* N > 1 (torchrun, one rank per GPU, NCCL): config 5 -- 4800 UHD frames (8
+  segments G(10..17)) split into contiguous ranges of 4800 / N frames, each rank
+  with a one-frame halo, the per-frame records all-gathered over NCCL (strong
+  scaling); per-rank kernel / gather times and the rank skew are reported.
 
 A step = one vca_analyze over the rank's whole batch (block kernel + finalize
 kernel) [+ the gather for N > 1]; frames are device-resident (7.46 GB per
@@ -49,13 +51,18 @@ def load_peaks():
 
 
 def load_traffic(workload):
-    """Per-launch DRAM bytes of the block kernel from the committed ncu summary."""
+    """Per-frame DRAM bytes of the block kernel from the committed ncu capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py from a `--set full` report),
+    with the capture it came from (report, git commit of the captured build)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
             d = json.load(fh)
         e = d.get(workload)
-        return None if e is None else float(e["dram_bytes_per_frame"])
+        if e is None:
+            return None
+        return {"bytes_per_frame": float(e["dram_bytes_per_frame"]),
+                "source": {k: e.get(k) for k in ("report", "git", "frames", "date")}}
     except Exception:
         return None
 
@@ -173,7 +180,8 @@ def cpu_oracle_fps(Y, U, V, bd, block, lowpass, target_s=10.0, max_frames=None, 
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle on the box's host cores, rank 0 only."""
+    """--impl reference: the CPU oracle on the box's host cores, rank 0 only, on a bounded sample
+    of our arm's workload (config 3 at N = 1, config 5 at N > 1)."""
     if rank != 0:
         return 0
     import oracle
@@ -181,11 +189,12 @@ def run_reference(args, rank, world):
     from paper_2304_12384_b200 import synth
 
     oracle.build()
-    c = synth.CONFIGS[3]
+    cfg_id = 3 if world == 1 else 5
+    c = synth.CONFIGS[cfg_id]
     cores = os.cpu_count() or 1
     # bounded sample of the workload: one frame per host core per step
     n = max(1, min(cores, 16))
-    Y, U, V = synth.config_frames(3, device="cpu", n_frames=n)
+    Y, U, V = synth.config_frames(cfg_id, device="cpu", n_frames=n)
     npl = synth.as_numpy_planes(Y, U, V)
     for _ in range(args.warmup):
         oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_threads=cores)
@@ -194,13 +203,14 @@ def run_reference(args, rank, world):
         oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_threads=cores)
     dt = time.perf_counter() - t0
     fps = n * args.steps / dt
-    sample = "%d UHD frames of config 3 per step (one per host core), oracle OpenMP over frames" % n
+    sample = "%d UHD frames of config %d per step (one per host core), oracle OpenMP over frames" % (n, cfg_id)
+    workload = "config3_uhd_8bit_lowpass32" if world == 1 else "config5_uhd_8bit_lowpass32_x4800"
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
-        "data": "synthetic (config 3 generator G(2), CPU torch)",
-        "config": {"workload": "config3_uhd_8bit_lowpass32 (bounded sample)", "width": c.width,
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "dtype": "int64+f64", "data": "synthetic (config %d generator, CPU torch)" % cfg_id,
+        "config": {"workload": workload + " (bounded sample)", "width": c.width,
                    "height": c.height, "bit_depth": 8, "block": 32, "lowpass": True, "frames_per_step": n},
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -210,17 +220,71 @@ def run_reference(args, rank, world):
     return 0
 
 
+def records_digest(rec):
+    """sha256 of the records' bytes (POC order): equal digests = bit-identical records."""
+    import hashlib
+
+    return hashlib.sha256(rec.tobytes()).hexdigest()
+
+
+def config5_single_gpu(dev, steps=5, warmup=3):
+    """fps_1 of config 5 as BASELINE.json defines the scaling baseline: all 4800 frames on ONE GPU
+    (59.7 GB resident), one vca_analyze call per step, CUDA events on the launching stream."""
+    import torch
+
+    from paper_2304_12384_b200 import Analyzer, records_to_numpy, synth
+
+    c = synth.CONFIGS[5]
+    t0 = time.perf_counter()
+    Y, U, V = synth.config_frames(5, device=dev, n_frames=c.n_frames)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    an = Analyzer(c.width, c.height, 8, c.block_size, c.lowpass)
+    out = torch.empty((c.n_frames, 8), dtype=torch.float64, device=dev)
+    scratch = torch.empty(an.scratch_bytes(c.n_frames) // 8 + 1, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        an.reset(0)
+        an.analyze(Y, U, V, out=out, scratch=scratch, stream=st)
+    torch.cuda.synchronize()
+    an.profile_read()
+    an.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        an.reset(0)
+        an.analyze(Y, U, V, out=out, scratch=scratch, stream=st)
+    e1.record(st)
+    torch.cuda.synchronize()
+    an.profile_enable(False)
+    ms = e0.elapsed_time(e1)
+    blk, fin, launches = an.profile_read()
+    rec = records_to_numpy(out)
+    res = {"value": c.n_frames * steps / (ms / 1e3), "unit": "frames/s", "frames": c.n_frames, "steps": steps,
+           "warmup": warmup, "ms_per_step": ms / steps, "kernel_ms_per_step": blk / steps,
+           "finalize_ms_per_step": fin / steps, "gpu_launches": int(launches),
+           "records_sha256": records_digest(rec), "generate_s": gen_s,
+           "note": "the same 4800 frames that --gpus N splits into contiguous ranges (strong scaling); "
+                   "records_sha256 equals the N > 1 line's when the sharded records are bit-identical"}
+    del Y, U, V, scratch
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--frames", type=int, default=SEG, help="frames per GPU (default 600)")
-    ap.add_argument("--config", type=int, default=0, help="override workload config (1-4; N=1 only)")
+    ap.add_argument("--frames", type=int, default=0, help="frames at N = 1 (default: the config's batch)")
+    ap.add_argument("--config", type=int, default=0, help="override the N = 1 workload config (1-4)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg")
-    ap.add_argument("--e2e-frames", type=int, default=120)
+    ap.add_argument("--no-config5", action="store_true", help="skip the N = 1 config-5 (4800-frame) leg")
+    ap.add_argument("--e2e-frames", type=int, default=0, help="frames of the e2e leg (default: the whole batch)")
+    ap.add_argument("--verify", action="store_true",
+                    help="N > 1: rank 0 re-analyses all 4800 frames on one context and compares the records")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -251,25 +315,27 @@ def main():
             dist.init_process_group(backend)
     red_dev = dev if backend == "nccl" else torch.device("cpu")
 
-    cfg_id = args.config or 3
-    c = synth.CONFIGS[cfg_id]
-    W, H, bd = c.width, c.height, c.bit_depth
-    F = args.frames
-    # --- inputs (outside timing).  N > 1: config 5's first N segments (N x 600 frames),
-    # contiguous POC ranges per rank with a one-frame halo (paper_2304_12384_b200.shard)
+    # --- inputs (outside timing)
+    #  N = 1: config 3, the metric's headline configuration (600 UHD frames).
+    #  N > 1: config 5 as BASELINE.json defines it -- its 4800 frames split into contiguous POC
+    #  ranges (shard.plan: 4800 / N per rank) with a one-frame halo, records gathered over NCCL
+    #  (strong scaling: the job is fixed, per-GPU work shrinks with N).
     if world == 1:
+        cfg_id = args.config or 3
+        c = synth.CONFIGS[cfg_id]
+        F = args.frames or c.n_frames
         Y, U, V = synth.config_frames(cfg_id, device=dev, n_frames=F)
-        n_halo = 0
-        workload = "config%d_%s_%df" % (cfg_id, c.name, F)
-        first_poc = 0
-        counts = None
+        n_halo, first_poc, counts = 0, 0, None
+        workload = "config%d_%s" % (cfg_id, c.name) + ("" if F == c.n_frames else "_%df" % F)
     else:
-        sh = shard.plan(world * F, world, rank)
-        n_halo = sh.n_halo
+        cfg_id = 5
+        c = synth.CONFIGS[5]
+        sh = shard.plan(c.n_frames, world, rank)
+        n_halo, first_poc = sh.n_halo, sh.first_poc
         Y, U, V = synth.config_frames(5, device=dev, n_frames=sh.n_frames, first_t=sh.first_frame)
-        workload = "config5_%s_%dx%df" % (synth.CONFIGS[5].name, world, F)
-        first_poc = sh.first_poc
-        counts = [shard.plan(world * F, world, r).count for r in range(world)]
+        workload = "config5_%s" % c.name
+        counts = [shard.plan(c.n_frames, world, r).count for r in range(world)]
+    W, H, bd = c.width, c.height, c.bit_depth
     torch.cuda.synchronize()
 
     an = Analyzer(W, H, bd, c.block_size, c.lowpass)
@@ -283,8 +349,9 @@ def main():
     gdone = [torch.cuda.Event(), torch.cuda.Event()]  # gather finished reading outs[b]
     gathered = [None]
     step_no = [0]
+    gev = []                                          # (start, end) events around each gather
 
-    def step():
+    def step(timed_gather=False):
         b = step_no[0] & 1
         out = outs[b]
         step_no[0] += 1
@@ -296,10 +363,19 @@ def main():
             if side is not None:
                 side.wait_stream(stream)
                 with torch.cuda.stream(side):
+                    if timed_gather:
+                        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                        ev[0].record(side)
                     gathered[0] = shard.gather_records(out, world, counts=counts)
+                    if timed_gather:
+                        ev[1].record(side)
+                        gev.append(ev)
                     gdone[b].record(side)
             else:
+                t0 = time.perf_counter()
                 gathered[0] = shard.gather_records(out, world, counts=counts)
+                if timed_gather:
+                    gev.append(time.perf_counter() - t0)
 
     for _ in range(args.warmup):
         step()
@@ -309,6 +385,7 @@ def main():
     clk_box = [None]
 
     def timed():
+        gev.clear()
         an.profile_enable(True)
         clk = ClockSampler(dev_index)
         clk_box[0] = clk
@@ -320,7 +397,7 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            step()
+            step(timed_gather=True)
         if side is not None:
             stream.wait_stream(side)  # the timed region ends after the last gather too
         e1.record(stream)
@@ -331,54 +408,70 @@ def main():
         an.profile_enable(False)
         ms = e0.elapsed_time(e1)
         blk_ms, fin_ms, launches = an.profile_read()
-        return ms, blk_ms, fin_ms, launches, clocks
+        g_ms = sum(e[0].elapsed_time(e[1]) if isinstance(e, tuple) else 1e3 * e for e in gev)
+        return ms, blk_ms, fin_ms, launches, clocks, g_ms
 
-    ms, blk_ms, fin_ms, launches, clocks = timed()
+    ms, blk_ms, fin_ms, launches, clocks, g_ms = timed()
     remeasured = False
     if bad_clocks(clocks):
         remeasured = True
-        ms, blk_ms, fin_ms, launches, clocks = timed()
+        ms, blk_ms, fin_ms, launches, clocks, g_ms = timed()
+    per_rank = None
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        mine = torch.tensor([ms, blk_ms, fin_ms, g_ms, float(nfr - n_halo)], dtype=torch.float64, device=red_dev)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per_rank = [{"rank": r, "ms_per_step": float(v[0]) / args.steps, "kernel_ms_per_step": float(v[1]) / args.steps,
+                     "finalize_ms_per_step": float(v[2]) / args.steps, "gather_ms_per_step": float(v[3]) / args.steps,
+                     "frames": int(v[4])} for r, v in enumerate(allr)]
+        ms = max(float(v[0]) for v in allr)        # max over ranks
 
-    frames_total = world * (nfr - n_halo) if world > 1 else nfr
+    frames_total = c.n_frames if world > 1 else nfr
     value = frames_total * args.steps / (ms / 1e3)
     fb = frame_bytes(W, H, bd)
     peak, peak_src = load_peaks()
     per_launch_s = blk_ms / 1e3 / args.steps
     achieved = nfr * fb / per_launch_s / 1e9
-    traffic_pf = load_traffic(workload.split("_")[0] if world == 1 else "config5")
+    traffic = load_traffic("config%d" % cfg_id)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8 in; s8xu8->s32 DCT, f64 features",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None, "dtype": "u8 in; s8xu8->s32 DCT, f64 features" if bd == 8
+        else "u16 in; f16/s8xu8 exact DCT -> s32, f64 features",
         "data": "synthetic, seeded (paper_2304_12384_b200/synth.py), device-resident",
         "config": {"workload": workload, "width": W, "height": H, "bit_depth": bd, "block": c.block_size,
-                   "lowpass": c.lowpass, "frames_per_gpu": nfr - n_halo, "halo_frames": n_halo,
-                   "path": an.info["path"], "parallelism": "frame-range dp%d + halo + %s all_gather" % (world, backend.upper())
-                   if world > 1 else "single GPU",
+                   "lowpass": c.lowpass, "frames_total": frames_total, "frames_per_gpu": nfr - n_halo,
+                   "halo_frames": n_halo,
+                   "path": an.info["path"], "parallelism": "frame-range dp%d + halo + %s all_gather"
+                   % (world, backend.upper()) if world > 1 else "single GPU",
                    "l2": "inputs %.2f GB per GPU > 126 MB L2; no flush needed" % (nfr * fb / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "frac_vs_8tbs_spec": achieved / 8000.0,
-                     "traffic": None if traffic_pf is None else traffic_pf * nfr,
-                     "kernel": "block kernel (A1-A7), CUDA events on the launching stream",
+                     "traffic": None if traffic is None else traffic["bytes_per_frame"] * nfr,
+                     "traffic_source": None if traffic is None else traffic["source"],
+                     "kernel": "block kernel (A1-A7), CUDA events on the launching stream"
+                               + (" (rank 0; per_rank has every rank)" if world > 1 else ""),
                      "algorithmic_bytes_per_launch": nfr * fb, "peak_source": peak_src,
                      "kernel_ms_per_launch": per_launch_s * 1e3, "finalize_ms_per_launch": fin_ms / args.steps,
-                     "roofline_fps": peak * 1e9 / fb},
+                     "roofline_fps": peak * 1e9 / fb * world},
         "gpu_launches": int(launches),
         "clocks": {**clocks, "remeasured": remeasured},
-        "energy": energy_line(clk_box[0], frames_total * args.steps if world == 1 else (nfr - n_halo) * args.steps),
+        "energy": energy_line(clk_box[0], (nfr - n_halo) * args.steps),
         "paper_context_fps": PAPER_FPS,
     }
+    if per_rank is not None:
+        steps_ms = [r["ms_per_step"] for r in per_rank]
+        line["per_rank"] = per_rank
+        line["rank_skew"] = max(steps_ms) / min(steps_ms)
 
     # --- e2e through the public host API (pinned host frames, H2D + D2H inside the timed region)
     if not args.no_e2e:
-        ne = min(args.e2e_frames, nfr)
+        ne = min(args.e2e_frames or nfr, nfr)
         hY, hU, hV = (p[:ne].cpu().pin_memory() for p in (Y, U, V))
         ae = Analyzer(W, H, bd, c.block_size, c.lowpass)
         chunk = int(os.environ.get("VCA_E2E_CHUNK", "8"))
+        ae.reset(first_poc)
         ae.analyze_host(hY, hU, hV, n_halo=n_halo, chunk_frames=chunk)  # warm-up / staging allocation
         if world > 1:
             dist.barrier()
@@ -406,7 +499,7 @@ def main():
         fr = (world if world > 1 else 1) * (ne - n_halo)
         line["e2e"] = {"value": fr * e_steps / dt, "unit": "frames/s", "h2d_bytes_per_step": ne * fb,
                        "d2h_bytes_per_step": (ne - n_halo) * 64, "frames_per_step": ne,
-                       "h2d_gbs": ne * fb * e_steps / dt / 1e9 / (world if world > 1 else 1),
+                       "h2d_gbs": ne * fb * e_steps / dt / 1e9,
                        "h2d_copy_gbs": h2d_peak,
                        "bound": "PCIe host-to-device copy of the frames (the kernels take < 1 % of the time)",
                        "api": "vca_analyze_host (pinned host memory, %d-frame chunks, copy/compute overlap)" % chunk}
@@ -425,13 +518,35 @@ def main():
         line["cpu_baseline_1thread"] = {"value": fps1, "unit": "frames/s", "cores": 1, "kind": "oracle",
                                         "sample": "%d frame analyses (passes over the first 8 frames), %.1f s"
                                                   % (n1, dt1)}
+    torch.cuda.synchronize()
+    rec = records_to_numpy(gathered[0] if world > 1 else outs[(step_no[0] - 1) & 1])
     if rank == 0:
-        # parity spot check of the timed output (first and last record) is done in tests; here sanity only
-        torch.cuda.synchronize()
-        rec = records_to_numpy(gathered[0] if world > 1 else outs[(step_no[0] - 1) & 1])
         assert np.array_equal(rec["poc"], np.arange(len(rec))), "records out of POC order"
         line["sanity"] = {"records": int(len(rec)), "first_poc": int(rec["poc"][0]), "last_poc": int(rec["poc"][-1]),
-                          "mean_E_Y": float(rec["E_Y"].mean())}
+                          "mean_E_Y": float(rec["E_Y"].mean()), "records_sha256": records_digest(rec)}
+
+    # --- N = 1: fps_1 on config 5's own 4800 frames (the strong-scaling baseline)
+    if world == 1 and not args.no_config5 and not args.config:
+        del Y, U, V, scratch, outs
+        torch.cuda.empty_cache()
+        line["config5_1gpu_4800"] = config5_single_gpu(dev)
+    # --- N > 1 --verify: rank 0 re-analyses the whole sequence on one context, segment by segment
+    if world > 1 and args.verify:
+        if rank == 0:
+            del Y, U, V
+            torch.cuda.empty_cache()
+            one = Analyzer(W, H, bd, c.block_size, c.lowpass)
+            parts = []
+            S = synth.SEGMENT_FRAMES
+            for seg in range(c.n_frames // S):
+                y, u, v = synth.config_frames(5, device=dev, n_frames=S, first_t=seg * S)
+                parts.append(records_to_numpy(one.analyze(y, u, v)))
+                del y, u, v
+            ref = np.concatenate(parts)
+            line["verify"] = {"single_context_sha256": records_digest(ref),
+                              "identical": bool(ref.tobytes() == rec.tobytes())}
+        dist.barrier()
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -158,16 +158,47 @@ int vca_profile_enable(vca_ctx *ctx, int enable);
 int vca_profile_read(vca_ctx *ctx, double *block_kernel_ms, double *finalize_ms, int64_t *launches);
 
 /* TEST-ONLY: analyse the single frame whose planes start at device
- * addresses planes[0..2] (rows pitch_bytes[p] apart) with exactly the
- * production block kernel of this context, and copy to host, for every
- * plane p with a non-NULL coeffs[p]: coeffs[p][k][i][j] (int32; C_00 is
- * stored mod 2^32, R-11) for every block k in raster order, sumx[p][k]
- * (sum of the samples entering the DCT), H[p][k] and L[p][k].  Host arrays
- * hold count[p] * n[p]^2, count[p], count[p] and count[p] entries.
- * Does not touch the carried state.  Synchronises the device. */
+ * addresses planes[0..2] (rows pitch_bytes[p] apart) with the DUMP
+ * instantiation of this context's block kernel (the production kernel's
+ * source with test outputs added; vca_debug_analyze ties its results to the
+ * production instantiation bit for bit), and copy to host, for every plane p
+ * with a non-NULL coeffs[p]: coeffs[p][k][i][j] (int32; C_00 is stored mod
+ * 2^32, R-11) for every block k in raster order and, where the pointer is
+ * non-NULL, sumx[p][k] (sum of the samples entering the DCT), H[p][k] and
+ * L[p][k].  Host arrays hold count[p] * n[p]^2, count[p], count[p] and
+ * count[p] entries.  Planes with a NULL coeffs[p] are not dumped.  The four
+ * pointer arrays themselves must be non-NULL (VCA_ERR_INVALID_ARG).  Does not
+ * touch the carried state.  Synchronises the device. */
 int vca_debug_dump(vca_ctx *ctx, const void *const planes[3], const int64_t pitch_bytes[3],
                    int32_t *const coeffs[3], int64_t *const sumx[3], double *const H[3],
                    double *const L[3]);
+
+/* TEST-ONLY: exactly vca_analyze (same arguments, records, scratch contents,
+ * carried state and errors), run through the DUMP instantiation of the block
+ * kernel, which additionally writes, for every block k of every frame t
+ * (index t * count[p] + k) of every plane p whose pointer is non-NULL, into
+ * caller-owned DEVICE arrays of n_frames * count[p] entries:
+ *   chk_dev[p]:  sum over (i,j) != (0,0) of C_ij * (i * n[p] + j + 1), the
+ *                exact AC checksum (int64, wrapping; the library zeroes the
+ *                array first, on `stream`);
+ *   sumx_dev[p]: sum of the DCT input samples (= C_00 / 4096, R-2);
+ *   H_dev[p]:    the block's texture energy H (A5).
+ * Records and scratch must equal vca_analyze's bit for bit on the same input
+ * (tests/test_parity_gpu.py); the per-block integers pin every coefficient of
+ * every block against the oracle (SURVEY 8(c) "Whole pipeline").  chk_dev,
+ * sumx_dev and H_dev may be NULL, or hold NULL entries. */
+int vca_debug_analyze(vca_ctx *ctx, const void *const planes[3], const int64_t pitch_bytes[3],
+                      const int64_t frame_stride_bytes[3], int n_frames, int n_halo, void *scratch,
+                      size_t scratch_bytes, vca_features *out_dev, int64_t *const chk_dev[3],
+                      int64_t *const sumx_dev[3], double *const H_dev[3], void *stream);
+
+/* TEST-ONLY (suite self-test): in a library built with -DVCA_MUTATE, add 1 to
+ * coefficient pos = i * n + j ((i,j) != (0,0)) of block `block` (global index
+ * t * count[plane] + k of the call) of plane `plane` in the kernel
+ * instantiations selected by `which` (bit 0: production, bit 1: DUMP), for
+ * every later launch in this process; plane -1 switches it off.  Returns
+ * VCA_ERR_INVALID_ARG in every other build. */
+int vca_debug_mutate(int plane, int64_t block, int pos, int which);
 
 void vca_destroy(vca_ctx *ctx);
 

@@ -60,6 +60,8 @@ def lib():
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.c_int]
+        P3 = ctypes.c_void_p * 3
+        L.vo_analyze_checks.argtypes = L.vo_analyze.argtypes + [P3, P3, P3]
         _lib = L
     return _lib
 
@@ -115,11 +117,13 @@ def block(plane: np.ndarray, bd: int, w: int, lowpass: bool, r: int, c: int):
 
 def analyze(Y: np.ndarray, U: np.ndarray, V: np.ndarray, bit_depth: int, block_size: int, lowpass: bool,
             n_halo: int = 0, prev_HY: np.ndarray | None = None, first_poc: int = 0,
-            want_HY: bool = False, n_threads: int = 0):
+            want_HY: bool = False, n_threads: int = 0, want_checks: bool = False):
     """Analyse frames [F][H][W] (Y) and [F][H/2][W/2] (U, V).
 
     Returns the structured record array (RECORD_DTYPE) for frames n_halo..F-1,
-    and with ``want_HY`` also the per-block luma energies [F][C_Y].
+    with ``want_HY`` also the per-block luma energies [F][C_Y], and with
+    ``want_checks`` also, per plane, {"chk", "sumx", "H"} arrays [F][C_p] of every
+    block's AC checksum sum_{(i,j)!=(0,0)} C_ij (i n + j + 1), sample sum and H.
     """
     planes = [np.ascontiguousarray(p) for p in (Y, U, V)]
     for p in planes:
@@ -140,9 +144,26 @@ def analyze(Y: np.ndarray, U: np.ndarray, V: np.ndarray, bit_depth: int, block_s
     if prev_HY is not None:
         prev = np.ascontiguousarray(prev_HY, dtype=np.float64)
         assert prev.shape == (CY,)
-    rc = lib().vo_analyze(ptrs, pitch, fstride, width, height, bit_depth, block_size, int(bool(lowpass)),
-                          F, n_halo, None if prev is None else prev.ctypes.data, first_poc,
-                          out.ctypes.data, None if HY is None else HY.ctypes.data, n_threads)
+    checks = None
+    args = [ptrs, pitch, fstride, width, height, bit_depth, block_size, int(bool(lowpass)),
+            F, n_halo, None if prev is None else prev.ctypes.data, first_poc,
+            out.ctypes.data, None if HY is None else HY.ctypes.data, n_threads]
+    if want_checks:
+        wc = chroma_block(w)
+        counts = [CY, block_count(width // 2, height // 2, wc), block_count(width // 2, height // 2, wc)]
+        checks = [{"chk": np.zeros((F, c), np.int64), "sumx": np.zeros((F, c), np.int64),
+                   "H": np.zeros((F, c), np.float64)} for c in counts]
+        P3 = ctypes.c_void_p * 3
+        rc = lib().vo_analyze_checks(*args, P3(*[d["chk"].ctypes.data for d in checks]),
+                                     P3(*[d["sumx"].ctypes.data for d in checks]),
+                                     P3(*[d["H"].ctypes.data for d in checks]))
+    else:
+        rc = lib().vo_analyze(*args)
     if rc:
         raise ValueError("vo_analyze -> %d" % rc)
-    return (out, HY) if want_HY else out
+    res = [out]
+    if want_HY:
+        res.append(HY)
+    if want_checks:
+        res.append(checks)
+    return res[0] if len(res) == 1 else tuple(res)

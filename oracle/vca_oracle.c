@@ -185,22 +185,40 @@ int64_t vo_block_count(int pw, int ph, int w)
     return (int64_t)((pw + w - 1) / w) * (int64_t)((ph + w - 1) / w);
 }
 
+/* Exact integer checks of one block's coefficients (test outputs, SURVEY 8(c)
+ * "Whole pipeline"): the AC checksum sum_{(i,j) != (0,0)} C_ij * (i n + j + 1),
+ * row-major; |C_ij| < 2^31 and n^2 <= 1024 terms, so the int64 sum is exact. */
+static int64_t vo_checksum(const int64_t *coeffs, int n)
+{
+    int64_t acc = 0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            if (i != 0 || j != 0) acc += coeffs[i * n + j] * (int64_t)(i * n + j + 1);
+    return acc;
+}
+
 /* Steps 1-5 for one plane of one frame: E_p, L_p and (optionally) the
- * per-block H vector in raster order. */
+ * per-block H vector in raster order, plus the optional per-block test
+ * outputs chk (vo_checksum), sx (sum of the DCT input samples) and Hb (H). */
 static int vo_plane(const uint8_t *plane, int64_t pitch, int bd, int pw, int ph, int w, int lowpass,
-                    double *E, double *Lp, double *Hvec)
+                    double *E, double *Lp, double *Hvec, int64_t *chk, int64_t *sx, double *Hb)
 {
     int n = lowpass ? w / 2 : w;
     int cols = (pw + w - 1) / w, rows = (ph + w - 1) / w;
     int64_t C = (int64_t)cols * rows;
     double sumH = 0.0, sumL = 0.0;
     int64_t k = 0;
+    int64_t coeffs[32 * 32];
     for (int r = 0; r < rows; ++r)
         for (int c = 0; c < cols; ++c, ++k) {
             double H, L;
-            int rc = vo_block(plane, pitch, bd, pw, ph, w, lowpass, r, c, NULL, NULL, &H, &L);
+            int64_t s = 0;
+            int rc = vo_block(plane, pitch, bd, pw, ph, w, lowpass, r, c, chk ? coeffs : NULL, &s, &H, &L);
             if (rc) return rc;
             if (Hvec) Hvec[k] = H;
+            if (chk) chk[k] = vo_checksum(coeffs, n);
+            if (sx) sx[k] = s;
+            if (Hb) Hb[k] = H;
             sumH += H;
             sumL += L;
         }
@@ -219,9 +237,26 @@ static int vo_plane(const uint8_t *plane, int64_t pitch, int bd, int pw, int ph,
  * Records are written for frames n_halo..n_frames-1 with poc = first_poc + i.
  * out_HY (optional) receives H_Y for all n_frames frames, [n_frames][C_Y].
  * n_threads <= 0 means the OpenMP default. */
+int vo_analyze_checks(const uint8_t *const planes[3], const int64_t pitch[3], const int64_t frame_stride[3],
+                      int width, int height, int bd, int block_size, int lowpass, int n_frames, int n_halo,
+                      const double *prev_HY, int64_t first_poc, vo_record *out, double *out_HY, int n_threads,
+                      int64_t *const chk[3], int64_t *const sx[3], double *const Hb[3]);
+
 int vo_analyze(const uint8_t *const planes[3], const int64_t pitch[3], const int64_t frame_stride[3],
                int width, int height, int bd, int block_size, int lowpass, int n_frames, int n_halo,
                const double *prev_HY, int64_t first_poc, vo_record *out, double *out_HY, int n_threads)
+{
+    return vo_analyze_checks(planes, pitch, frame_stride, width, height, bd, block_size, lowpass, n_frames,
+                             n_halo, prev_HY, first_poc, out, out_HY, n_threads, NULL, NULL, NULL);
+}
+
+/* vo_analyze plus optional per-block test outputs for every frame t and plane
+ * p with non-NULL chk/sx/Hb (arrays of n_frames * C_p entries, index
+ * t * C_p + k): the AC checksum, the sample sum and H of every block. */
+int vo_analyze_checks(const uint8_t *const planes[3], const int64_t pitch[3], const int64_t frame_stride[3],
+                      int width, int height, int bd, int block_size, int lowpass, int n_frames, int n_halo,
+                      const double *prev_HY, int64_t first_poc, vo_record *out, double *out_HY, int n_threads,
+                      int64_t *const chk[3], int64_t *const sx[3], double *const Hb[3])
 {
     if (!planes || !pitch || !frame_stride || !out) return VO_EINVAL;
     if (width < 2 || height < 2 || (width & 1) || (height & 1)) return VO_EINVAL;
@@ -253,8 +288,11 @@ int vo_analyze(const uint8_t *const planes[3], const int64_t pitch[3], const int
         for (int p = 0; p < 3; ++p) {
             const uint8_t *base = planes[p] + (int64_t)t * frame_stride[p];
             double E = 0.0, L = 0.0;
+            const int64_t Cp = vo_block_count(pw[p], ph[p], wp[p]);
+            const size_t o = (size_t)t * (size_t)Cp;
             int rc = vo_plane(base, pitch[p], bd, pw[p], ph[p], wp[p], lowpass, &E, &L,
-                              p == 0 ? HY + (size_t)t * (size_t)CY : NULL);
+                              p == 0 ? HY + (size_t)t * (size_t)CY : NULL, chk && chk[p] ? chk[p] + o : NULL,
+                              sx && sx[p] ? sx[p] + o : NULL, Hb && Hb[p] ? Hb[p] + o : NULL);
             if (rc) err = rc;
             feat[6 * t + 2 * p] = E;
             feat[6 * t + 2 * p + 1] = L;

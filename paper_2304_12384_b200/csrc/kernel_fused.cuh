@@ -919,6 +919,9 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
         for (int e = 0; e < 2; ++e) wcc[e] = U.wc[e];
     }
     double hY[NU];
+    int64_t ckY[NU], ckU[NU], ckV[NU];  // DUMP: per-lane AC checksum terms (tests)
+#pragma unroll
+    for (int n = 0; n < NU; ++n) ckY[n] = ckU[n] = ckV[n] = 0;
     // 8-bit low-pass on whole columns: the 2x2 sums run on the tensor cores (A3 as an
     // exact 0/1 contraction, rounding offset as the accumulator init)
     constexpr bool MMA_DS = F::LP && ES == 1 && !XPART && kMmaDownsample;
@@ -966,6 +969,18 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             else
                 dct16<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
         }
+        if (DUMP || kMutate) {
+#pragma unroll
+            for (int n = 0; n < NU; ++n)
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int pos = (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1);
+                        if (kMutate && pos) C[n][p][e] = mutate<DUMP>(C[n][p][e], 0, k[n], pos);
+                        if (DUMP && pos) ckY[n] += (int64_t)C[n][p][e] * (pos + 1);
+                    }
+        }
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             // |C| folds into the DFMA operand (fabs of an exact int32 -> double conversion)
@@ -977,7 +992,7 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             }
             hY[n] = h0 + h1;
             o[n].dcY = C[n][0][0];
-            if (DUMP) {
+            if (DUMP && a.dump.coeffs[0]) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -1035,12 +1050,15 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                     const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int32_t cc = combine3(E0[e], E1[e], E2[e]);
+                        int32_t cc = combine3(E0[e], E1[e], E2[e]);
+                        const int pos = (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1);
+                        if (kMutate && pos) cc = mutate<DUMP>(cc, 0, k[n], pos);
                         hacc[n][e] = fma(wv[e], fabs(i2d(cc)), hacc[n][e]);
                         if (mt == 0 && rr == 0 && e == 0) o[n].dcY = cc;
-                        if (DUMP)
-                            a.dump.coeffs[0][k[n] * 1024 + (16 * mt + g + 8 * (e >> 1)) * 32 + 8 * rr + 2 * t + (e & 1)] =
-                                cc;
+                        if (DUMP) {
+                            if (pos) ckY[n] += (int64_t)cc * (pos + 1);
+                            if (a.dump.coeffs[0]) a.dump.coeffs[0][k[n] * 1024 + pos] = cc;
+                        }
                     }
                 }
             }
@@ -1091,6 +1109,16 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             else
                 dct8pair<ES, MMA_DS>(L, blo[n], bhi[n], C[n]);
         }
+        if (DUMP || kMutate) {
+#pragma unroll
+            for (int n = 0; n < NU; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int pos = g * 8 + 2 * t + (e & 1);
+                    if (kMutate && pos) C[n][e] = mutate<DUMP>(C[n][e], 1 + (e >> 1), k[n], pos);
+                    if (DUMP && pos) (e < 2 ? ckU[n] : ckV[n]) += (int64_t)C[n][e] * (pos + 1);
+                }
+        }
 #pragma unroll
         for (int n = 0; n < NU; ++n) {
             if (ChromaAcc<F>::ON) {
@@ -1110,9 +1138,11 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
             }
             o[n].dcU = C[n][0];
             o[n].dcV = C[n][2];
-            if (DUMP) {
+            if (DUMP && a.dump.coeffs[1]) {
                 a.dump.coeffs[1][k[n] * 64 + g * 8 + 2 * t] = C[n][0];
                 a.dump.coeffs[1][k[n] * 64 + g * 8 + 2 * t + 1] = C[n][1];
+            }
+            if (DUMP && a.dump.coeffs[2]) {
                 a.dump.coeffs[2][k[n] * 64 + g * 8 + 2 * t] = C[n][2];
                 a.dump.coeffs[2][k[n] * 64 + g * 8 + 2 * t + 1] = C[n][3];
             }
@@ -1128,6 +1158,16 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                 for (int q = 0; q < 2; ++q) load4<F, 1>(box, ubC[n], 8 * q + g, t, hvC, wvC, XPART, blo[q], bhi[q]);
                 int32_t C[2][4];
                 dct16<ES>(L, blo, bhi, C);
+                if (DUMP || kMutate) {
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int pos = (g + 8 * (e >> 1)) * 16 + 8 * p + 2 * t + (e & 1);
+                            if (kMutate && pos) C[p][e] = mutate<DUMP>(C[p][e], pl, k[n], pos);
+                            if (DUMP && pos) (pl == 1 ? ckU[n] : ckV[n]) += (int64_t)C[p][e] * (pos + 1);
+                        }
+                }
                 double hacc = 0.0;
                 if (ChromaAcc<F>::ON) {
 #pragma unroll
@@ -1157,7 +1197,7 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                     o[n].dcV = C[0][0];
                     if (!ChromaAcc<F>::ON) hv_acc += hacc;
                 }
-                if (DUMP) {
+                if (DUMP && a.dump.coeffs[pl]) {
 #pragma unroll
                     for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -1177,19 +1217,19 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
                 hu += __shfl_xor_sync(0xffffffffu, hu, s);
                 hv += __shfl_xor_sync(0xffffffffu, hv, s);
             }
+            chk_add(a.dump.chk[0], k[n], ckY[n]);
+            chk_add(a.dump.chk[1], k[n], ckU[n]);
+            chk_add(a.dump.chk[2], k[n], ckV[n]);
             if (g == 0 && t == 0) {
-                const uint32_t sxY = (uint32_t)o[n].dcY >> 12, sxU = (uint32_t)o[n].dcU >> 12,
-                               sxV = (uint32_t)o[n].dcV >> 12;
+                const uint32_t sx[3] = {(uint32_t)o[n].dcY >> 12, (uint32_t)o[n].dcU >> 12, (uint32_t)o[n].dcV >> 12};
+                const double hh[3] = {hy, hu, hv};
                 const int64_t kk = k[n];
-                a.dump.sumx[0][kk] = sxY;
-                a.dump.sumx[1][kk] = sxU;
-                a.dump.sumx[2][kk] = sxV;
-                a.dump.H[0][kk] = hy;
-                a.dump.H[1][kk] = hu;
-                a.dump.H[2][kk] = hv;
-                a.dump.L[0][kk] = sqrt((double)sxY * (1.0 / NY));
-                a.dump.L[1][kk] = sqrt((double)sxU * (1.0 / NC));
-                a.dump.L[2][kk] = sqrt((double)sxV * (1.0 / NC));
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    if (a.dump.sumx[q]) a.dump.sumx[q][kk] = sx[q];
+                    if (a.dump.H[q]) a.dump.H[q][kk] = hh[q];
+                    if (a.dump.L[q]) a.dump.L[q][kk] = sqrt((double)sx[q] * (q == 0 ? 1.0 / NY : 1.0 / NC));
+                }
             }
         }
     }
@@ -1220,6 +1260,15 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
         load4<F, 0>(base + LYoff[p], LYub[p], g, t & 1, hvY, XPART ? wvY[p] : W, XPART && wvY[p] < W, lo, hi);
         int32_t C[4];
         dct8pair<ES>(L, lo, hi, C);
+        if (DUMP || kMutate) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t kk = k[2 * p + (e >> 1)];
+                const int pos = g * 8 + 2 * t + (e & 1);
+                if (kMutate && pos && kk >= 0) C[e] = mutate<DUMP>(C[e], 0, kk, pos);
+                if (DUMP && pos && kk >= 0) chk_add(a.dump.chk[0], kk, (int64_t)C[e] * (pos + 1));
+            }
+        }
         double h0 = fma(wc1, fabs(i2d(C[1])), wc0 * fabs(i2d(C[0])));
         double h1 = fma(wc1, fabs(i2d(C[3])), wc0 * fabs(i2d(C[2])));
         h0 += __shfl_xor_sync(0xffffffffu, h0, 1);
@@ -1230,7 +1279,7 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
         hY[2 * p + 1] = h1;
         dcY[2 * p] = C[0];
         dcY[2 * p + 1] = C[2];
-        if (DUMP) {
+        if (DUMP && a.dump.coeffs[0]) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int64_t kk = k[2 * p + (e >> 1)];
@@ -1244,6 +1293,16 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
         load4<F, 1>(base + LCoff, LCub, g & 3, 0, hvC, XPART ? wvC : WC, XPART && wvC < WC, lo, hi);
         int32_t C[4];
         dct4oct<ES>(L, lo, hi, C);
+        if (DUMP || kMutate) {
+            const int pl = 1 + (g >> 2);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int64_t kk = k[e < 2 ? (t >> 1) : 2 + (t >> 1)];
+                const int pos = (g & 3) * 4 + 2 * (t & 1) + (e & 1);
+                if (kMutate && pos && kk >= 0) C[e] = mutate<DUMP>(C[e], pl, kk, pos);
+                if (DUMP && pos && kk >= 0) chk_add(a.dump.chk[pl], kk, (int64_t)C[e] * (pos + 1));
+            }
+        }
         // lane's plane is fixed (g >> 2); slots e and e + 2 share a weight (different units)
         const uint32_t s0 = (uint32_t)abs(C[0]) + (uint32_t)abs(C[2]);
         const uint32_t s1 = (uint32_t)abs(C[1]) + (uint32_t)abs(C[3]);
@@ -1261,7 +1320,7 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int64_t kk = k[e < 2 ? (t >> 1) : 2 + (t >> 1)];
-                if (kk >= 0) a.dump.coeffs[pl][kk * 16 + (g & 3) * 4 + 2 * (t & 1) + (e & 1)] = C[e];
+                if (kk >= 0 && a.dump.coeffs[pl]) a.dump.coeffs[pl][kk * 16 + (g & 3) * 4 + 2 * (t & 1) + (e & 1)] = C[e];
             }
             // per-block chroma H: this lane's weighted terms, reduced over the warp per (unit, plane)
 #pragma unroll
@@ -1275,7 +1334,7 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
                     }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if ((g | t) == 0 && k[n] >= 0) a.dump.H[1 + q][k[n]] = v;
+                    if ((g | t) == 0 && k[n] >= 0 && a.dump.H[1 + q]) a.dump.H[1 + q][k[n]] = v;
                 }
             // per-block chroma DC sums and L (lane (4q, 2 (n & 1)) holds unit n's plane-q DC)
             if ((g & 3) == 0 && (t & 1) == 0) {
@@ -1285,8 +1344,8 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
                     const int n = m == 0 ? (t >> 1) : 2 + (t >> 1);
                     if (k[n] >= 0) {
                         const uint32_t sx = (uint32_t)dcC[m] >> 12;
-                        a.dump.sumx[1 + q][k[n]] = sx;
-                        a.dump.L[1 + q][k[n]] = sqrt((double)sx * (1.0 / F::NC));
+                        if (a.dump.sumx[1 + q]) a.dump.sumx[1 + q][k[n]] = sx;
+                        if (a.dump.L[1 + q]) a.dump.L[1 + q][k[n]] = sqrt((double)sx * (1.0 / F::NC));
                     }
                 }
             }
@@ -1300,9 +1359,9 @@ __device__ __forceinline__ void process_group8(const UnitCtx<F> &U, const FusedA
             for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             if ((g | t) == 0 && k[n] >= 0) {
                 const uint32_t sx = (uint32_t)dcY[n] >> 12;
-                a.dump.H[0][k[n]] = v;
-                a.dump.sumx[0][k[n]] = sx;
-                a.dump.L[0][k[n]] = sqrt((double)sx * (1.0 / F::NY));
+                if (a.dump.H[0]) a.dump.H[0][k[n]] = v;
+                if (a.dump.sumx[0]) a.dump.sumx[0][k[n]] = sx;
+                if (a.dump.L[0]) a.dump.L[0][k[n]] = sqrt((double)sx * (1.0 / F::NY));
             }
         }
     }
@@ -1535,6 +1594,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
         for (int e = 0; e < ChromaAcc<F>::NP; ++e) ca.u[e] = ca.v[e] = 0u;
         double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // identical in all lanes
         double *HYrow = a.s.HY + (int64_t)f * CY + (int64_t)r * cols;
+        const int64_t fCY = (int64_t)f * CY;  // global index of the frame's first block (test outputs)
         // strips in chroma-flush windows of SPC: the flush runs once after each window (as its
         // own block, not if-converted into predicated instructions issued on every strip:
         // config 3 +1 %, config 4 +3.5 %, w = 16 full +7 %).  The n = 8 families keep the
@@ -1568,7 +1628,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     int64_t kk[4];
 #pragma unroll
                     for (int n = 0; n < 4; ++n)
-                        kk[n] = (DUMP && cm + 4 * n < cols) ? (int64_t)r * cols + cm + 4 * n : -1;
+                        kk[n] = ((DUMP || kMutate) && cm + 4 * n < cols) ? fCY + (int64_t)r * cols + cm + 4 * n : -1;
                     if (s < s_fast) {
                         const int wY[2] = {W, W};
                         process_group8<F, false, DUMP>(U, a, base, LYoff[m], LYub[m], LCoff[m], LCub[m], hvY, hvC, wY,
@@ -1605,7 +1665,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                 for (int n = 0; n < NU; ++n) {
                     bY[n] = base + offY[n];
                     bU[n] = base + offU[n];
-                    kk[n] = DUMP ? (int64_t)r * cols + c0 + 4 * n : 0;
+                    kk[n] = (DUMP || kMutate) ? fCY + (int64_t)r * cols + c0 + 4 * n : 0;
                 }
                 process_units<F, false, DUMP, NU>(U, a, bY, bU, ubYc, ubCc, hvY, hvC, W, WC, kk, o, hu, hv, ca);
                 // stash: per-unit luma row-group partials and raw C_00 values, reduced SPF strips
@@ -1626,7 +1686,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     const uint32_t bY[1] = {base + (v / F::UPB_Y) * F::BOXB_Y};
                     const uint32_t bU[1] = {base + F::ST_Y + (v / F::UPB_C) * F::BOXB_C};
                     const int uY[1] = {v % F::UPB_Y}, uC[1] = {v % F::UPB_C};
-                    const int64_t kk[1] = {(int64_t)r * cols + c};
+                    const int64_t kk[1] = {fCY + (int64_t)r * cols + c};
                     const int wvY = min(W, a.width[0] - c * W), wvC = min(WC, a.width[1] - c * WC);
                     UnitOut o1[1];
                     if (wvY < W)
@@ -1803,7 +1863,7 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     a.T_all = T;
     a.s = s;
     a.dump = dp;
-    const bool dump = dp.coeffs[0] != nullptr;
+    const bool dump = dp.on != 0;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
     // CTAs per SM: a property of the kernel and the device, queried once per instantiation
     // (the query costs microseconds of host time on every call otherwise)
@@ -1821,6 +1881,26 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     if (grid > items) grid = items;
     kern<<<(unsigned)grid, F::THREADS, Lay<F>::SMEM, st>>>(mY, mU, mV, a);
     return 0;
+}
+
+template <int W, int BD, int LP>
+inline bool check_one(const Planes3 &pl, int n_frames)
+{
+    using F = Fam<W, BD, LP>;
+    CUtensorMap m;
+    return make_map(&m, pl.p[0], n_frames, F::ES, F::IB_Y, W) && make_map(&m, pl.p[1], n_frames, F::ES, F::IB_C, W / 2) &&
+           make_map(&m, pl.p[2], n_frames, F::ES, F::IB_C, W / 2) && (int64_t)n_frames * pl.p[0].rows <= 0x7fffffff;
+}
+
+// True if launch_fused would accept these planes (tensor maps encodable, item count in range).
+inline bool fused_check(const Planes3 &pl, int n_frames, int bd, int lowpass)
+{
+    const int w = pl.p[0].w;
+    if (w == 32 && lowpass) return bd == 8 ? check_one<32, 8, 1>(pl, n_frames) : check_one<32, 10, 1>(pl, n_frames);
+    if (w == 32) return bd == 8 ? check_one<32, 8, 0>(pl, n_frames) : check_one<32, 10, 0>(pl, n_frames);
+    if (w == 16 && lowpass) return bd == 8 ? check_one<16, 8, 1>(pl, n_frames) : check_one<16, 10, 1>(pl, n_frames);
+    if (w == 8) return bd == 8 ? check_one<8, 8, 0>(pl, n_frames) : check_one<8, 10, 0>(pl, n_frames);
+    return bd == 8 ? check_one<16, 8, 0>(pl, n_frames) : check_one<16, 10, 0>(pl, n_frames);
 }
 
 // Returns 0 on launch, -1 on a CUDA launch failure (see cudaGetLastError), -2 if a

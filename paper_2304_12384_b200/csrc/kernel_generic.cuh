@@ -17,12 +17,50 @@ struct Planes3 {
     PlaneDesc p[3];
 };
 
+// Test-only outputs of the DUMP kernel instantiations (vca_debug_dump, vca_debug_analyze).
+// Every array is indexed by the block's global index t * count[p] + k (frame t, raster block
+// k); a NULL pointer is never written.  chk accumulates, with integer atomics (exact and
+// order-independent), the checksum sum_{(i,j) != (0,0)} C_ij (i n + j + 1) mod 2^64 of each
+// block's AC coefficients; the host zeroes it first.
 struct DumpPtrs {
-    int32_t *coeffs[3];
-    int64_t *sumx[3];
-    double *H[3];
-    double *L[3];
+    int on;                     // launch the DUMP instantiation
+    int32_t *coeffs[3];         // [F][C_p][n][n] (C_00 mod 2^32, R-11)
+    int64_t *sumx[3];           // [F][C_p] sum of the DCT input samples (= C_00 / 4096)
+    double *H[3];               // [F][C_p] texture energy
+    double *L[3];               // [F][C_p] luminescence
+    unsigned long long *chk[3];  // [F][C_p] AC checksum
 };
+
+__device__ __forceinline__ void chk_add(unsigned long long *chk, int64_t idx, int64_t v)
+{
+    if (chk && v) atomicAdd(chk + idx, (unsigned long long)v);
+}
+
+// Coefficient mutation for the suite's self-test (tests/test_mutation_gpu.py): a VCA_MUTATE
+// build adds 1 to the coefficient at position pos of block `block` (global index) of plane
+// `plane` in the instantiations selected by `which` (bit 0 production, bit 1 DUMP), as set by
+// vca_debug_mutate.  Default builds compile mutate() to the identity.
+#ifdef VCA_MUTATE
+struct MutSpec {
+    int plane, which, pos;
+    long long block;
+};
+__device__ MutSpec vca_mut = {-1, 0, -1, -1};
+constexpr bool kMutate = true;
+template <bool DUMP>
+__device__ __forceinline__ int32_t mutate(int32_t c, int plane, int64_t block, int pos)
+{
+    const MutSpec m = vca_mut;
+    return (m.plane == plane && m.block == block && m.pos == pos && (m.which & (DUMP ? 2 : 1))) ? c + 1 : c;
+}
+#else
+constexpr bool kMutate = false;
+template <bool DUMP>
+__device__ __forceinline__ int32_t mutate(int32_t c, int, int64_t, int)
+{
+    return c;
+}
+#endif
 
 template <int BD>
 __device__ __forceinline__ int load_sample(const uint8_t *frame, const PlaneDesc &P, int x, int y)
@@ -90,17 +128,21 @@ generic_block_kernel(Planes3 planes, int n_frames, int lowpass, const int8_t *__
         __syncwarp();
         // A4 second pass: C[i][j] = sum_x Z[i][x] T[j][x] (int64), then A5
         double hacc = 0.0;
-        int64_t c00 = 0;
+        int64_t c00 = 0, ck = 0;
+        const int64_t kg = f * P.count + k;  // global block index of the test outputs
         for (int idx = lane; idx < n * n; idx += 32) {
             const int i = idx / n, j = idx - (idx / n) * n;
             int64_t acc = 0;
             for (int x = 0; x < n; ++x) acc += (int64_t)Z[i][x] * (int64_t)__ldg(T + j * n + x);
+            if (kMutate && idx != 0) acc = dump.on ? mutate<true>((int32_t)acc, p, kg, idx) : mutate<false>((int32_t)acc, p, kg, idx);
             if (idx == 0) c00 = acc;
+            else ck += acc * (idx + 1);
             const int64_t a = acc < 0 ? -acc : acc;
             hacc += __ldg(W + idx) * (double)a;   // W(0,0) = 0 excludes DC
             if (dump.coeffs[p])
-                dump.coeffs[p][k * n * n + idx] = (int32_t)(uint32_t)(uint64_t)acc;
+                dump.coeffs[p][kg * n * n + idx] = (int32_t)(uint32_t)(uint64_t)acc;
         }
+        if (dump.on) chk_add(dump.chk[p], kg, ck);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) hacc += __shfl_xor_sync(0xffffffffu, hacc, o);
         if (lane == 0) {
@@ -110,11 +152,9 @@ generic_block_kernel(Planes3 planes, int n_frames, int lowpass, const int8_t *__
             pp[0] = hacc;
             pp[1] = L;
             if (p == 0) s.HY[f * C0 + k] = hacc;
-            if (dump.sumx[p]) {
-                dump.sumx[p][k] = sumx;
-                dump.H[p][k] = hacc;
-                dump.L[p][k] = L;
-            }
+            if (dump.sumx[p]) dump.sumx[p][kg] = sumx;
+            if (dump.H[p]) dump.H[p][kg] = hacc;
+            if (dump.L[p]) dump.L[p][kg] = L;
         }
         __syncwarp();
     }
@@ -233,26 +273,36 @@ small_block_kernel(Planes3 planes, int n_frames, const int8_t *__restrict__ T_al
                 }
                 // A4 vertical pass, A5 (row-major, DC excluded)
                 int c00 = 0;
+                int64_t ck = 0;
+                const int64_t kg = (int64_t)f * Cp + k;  // global block index of the test outputs
                 int32_t *dco = nullptr;
                 if (DUMP) dco = p == 0 ? dump.coeffs[0] : p == 1 ? dump.coeffs[1] : dump.coeffs[2];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int cij = T[i][0] * Z[0][j] + T[i][1] * Z[1][j] + T[i][2] * Z[2][j] + T[i][3] * Z[3][j];
+                        int cij = T[i][0] * Z[0][j] + T[i][1] * Z[1][j] + T[i][2] * Z[2][j] + T[i][3] * Z[3][j];
+                        if (kMutate && (i | j)) cij = mutate<DUMP>(cij, p, kg, i * 4 + j);
                         if (i == 0 && j == 0) c00 = cij;
                         else hb = fma(Wt[i][j], (double)(cij < 0 ? -cij : cij), hb);
-                        if (DUMP) dco[(int64_t)k * 16 + i * 4 + j] = cij;
+                        if (DUMP) {
+                            if (i | j) ck += (int64_t)cij * (i * 4 + j + 1);
+                            if (dco) dco[kg * 16 + i * 4 + j] = cij;
+                        }
                     }
                 const int64_t sumx = c00 >> 12;         // C_00 = 4096 * sum(X) exactly
                 const double Lb = sqrt((double)sumx / 4.0);  // A6
                 h += hb;  // per lane: block b = 0, 1, ... in order
                 L += Lb;
                 if (p == 0) s.HY[(int64_t)f * C0 + k] = hb;
-                if (DUMP) {  // debug dump (all three planes are dumped together)
-                    (p == 0 ? dump.sumx[0] : p == 1 ? dump.sumx[1] : dump.sumx[2])[k] = sumx;
-                    (p == 0 ? dump.H[0] : p == 1 ? dump.H[1] : dump.H[2])[k] = hb;
-                    (p == 0 ? dump.L[0] : p == 1 ? dump.L[1] : dump.L[2])[k] = Lb;
+                if (DUMP) {  // test outputs (NULL planes are skipped)
+                    int64_t *sx = p == 0 ? dump.sumx[0] : p == 1 ? dump.sumx[1] : dump.sumx[2];
+                    double *hh = p == 0 ? dump.H[0] : p == 1 ? dump.H[1] : dump.H[2];
+                    double *ll = p == 0 ? dump.L[0] : p == 1 ? dump.L[1] : dump.L[2];
+                    if (sx) sx[kg] = sumx;
+                    if (hh) hh[kg] = hb;
+                    if (ll) ll[kg] = Lb;
+                    chk_add(p == 0 ? dump.chk[0] : p == 1 ? dump.chk[1] : dump.chk[2], kg, ck);
                 }
             }
         }

@@ -167,10 +167,7 @@ EventTriple take_events(vca_ctx *ctx, cudaError_t *err)
     return t;
 }
 
-// Enqueue one analysis of n_frames frames (validated) on `st`.
-int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pitch[3], const int64_t fstride[3],
-                    int n_frames, int n_halo, void *scratch, vca_features *out, cudaStream_t st,
-                    const DumpPtrs *dump)
+Planes3 make_planes(const vca_ctx *ctx, const void *const planes[3], const int64_t pitch[3], const int64_t fstride[3])
 {
     Planes3 pl;
     for (int p = 0; p < 3; ++p) {
@@ -179,6 +176,27 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         pl.p[p].pitch = pitch[p];
         pl.p[p].fstride = fstride[p];
     }
+    return pl;
+}
+
+// The argument checks launch_analysis makes before enqueuing anything (tensor maps encodable,
+// work counts in range), without launching: VCA_OK or VCA_ERR_INVALID_ARG.
+int validate_launch(const vca_ctx *ctx, const void *const planes[3], const int64_t pitch[3], const int64_t fstride[3],
+                    int n_frames)
+{
+    if (ctx->path == VCA_PATH_FUSED_MMA)
+        return fused_check(make_planes(ctx, planes, pitch, fstride), n_frames, ctx->bd, ctx->lowpass) ? VCA_OK
+                                                                                                       : VCA_ERR_INVALID_ARG;
+    const int64_t per_frame = ctx->geo[0].count + ctx->geo[1].count + ctx->geo[2].count;
+    return per_frame > 0x7fffffff ? VCA_ERR_INVALID_ARG : VCA_OK;
+}
+
+// Enqueue one analysis of n_frames frames (validated) on `st`.
+int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pitch[3], const int64_t fstride[3],
+                    int n_frames, int n_halo, void *scratch, vca_features *out, cudaStream_t st,
+                    const DumpPtrs *dump)
+{
+    const Planes3 pl = make_planes(ctx, planes, pitch, fstride);
     Scratch s;
     s.HY = static_cast<double *>(scratch);
     s.partial = s.HY + (size_t)n_frames * (size_t)ctx->geo[0].count;
@@ -212,7 +230,7 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
             int64_t tb = (chunks + 7) / 8;  // 8 warps per 256-thread CTA
             const int64_t tcap = (int64_t)ctx->sm_count * 8;
             if (tb > tcap) tb = tcap;
-            const bool dmp = dp.coeffs[0] != nullptr;
+            const bool dmp = dp.on != 0;
             if (ctx->bd == 8) {
                 if (dmp)
                     small_block_kernel<8, true><<<(unsigned)tb, 256, 0, st>>>(pl, n_frames, ctx->d_T, ctx->d_W, s, dp);
@@ -235,7 +253,7 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
     }
     VCA_CK(ctx, cudaGetLastError());
     ctx->launches += 1;
-    if (dump) return VCA_OK;  // test dump: no records, no state change
+    if (!out) return VCA_OK;  // vca_debug_dump: no records, no state change
     if (prof) VCA_CK(ctx, cudaEventRecord(ev.e[1], st));
 
     FinalizeArgs fa;
@@ -420,26 +438,30 @@ int vca_analyze_host(vca_ctx *ctx, const void *const host_planes[3], const int64
     // (re)allocate context-owned staging when the chunk grows
     const size_t need = frame_bytes * (size_t)chunk_frames;
     if (need > ctx->stage_bytes || chunk_frames > ctx->stage_frames) {
-        for (int b = 0; b < 2; ++b) {
-            if (ctx->stage[b]) cudaFree(ctx->stage[b]);
-            ctx->stage[b] = nullptr;
-        }
-        if (ctx->h_scratch) cudaFree(ctx->h_scratch);
-        ctx->h_scratch = nullptr;
-        for (int b = 0; b < 2; ++b) {
-            cudaError_t e = cudaMalloc(&ctx->stage[b], need);
-            if (e != cudaSuccess) {
-                cudaGetLastError();
-                ctx->stage_bytes = 0;
-                return e == cudaErrorMemoryAllocation ? VCA_ERR_OOM : fail_cuda(ctx, e);
+        // any failure leaves no staging at all (sizes 0, pointers NULL), so a later call
+        // reallocates instead of launching on a partial set of buffers
+        auto drop = [ctx]() {
+            for (int b = 0; b < 2; ++b) {
+                if (ctx->stage[b]) cudaFree(ctx->stage[b]);
+                ctx->stage[b] = nullptr;
             }
-        }
-        ctx->h_scratch_bytes = scratch_bytes(ctx, chunk_frames);
-        cudaError_t e = cudaMalloc(&ctx->h_scratch, 2 * ctx->h_scratch_bytes);
+            if (ctx->h_scratch) cudaFree(ctx->h_scratch);
+            ctx->h_scratch = nullptr;
+            ctx->stage_bytes = 0;
+            ctx->stage_frames = 0;
+            ctx->h_scratch_bytes = 0;
+        };
+        drop();
+        cudaError_t e = cudaSuccess;
+        for (int b = 0; b < 2 && e == cudaSuccess; ++b) e = cudaMalloc(&ctx->stage[b], need);
+        const size_t hsb = scratch_bytes(ctx, chunk_frames);
+        if (e == cudaSuccess) e = cudaMalloc(&ctx->h_scratch, 2 * hsb);
         if (e != cudaSuccess) {
             cudaGetLastError();
+            drop();
             return e == cudaErrorMemoryAllocation ? VCA_ERR_OOM : fail_cuda(ctx, e);
         }
+        ctx->h_scratch_bytes = hsb;
         ctx->stage_bytes = need;
         ctx->stage_frames = chunk_frames;
     }
@@ -468,6 +490,15 @@ int vca_analyze_host(vca_ctx *ctx, const void *const host_planes[3], const int64
     VCA_CK(ctx, cudaStreamWaitEvent(ctx->s_copy, start_ev, 0));
     VCA_CK(ctx, cudaStreamWaitEvent(ctx->s_comp, start_ev, 0));
 
+    // validate every chunk geometry (full chunks and the last, shorter one) before anything is
+    // enqueued, so an argument error leaves the context unchanged (vca.h)
+    {
+        const void *dpl[3] = {ctx->stage[0] + off[0], ctx->stage[0] + off[1], ctx->stage[0] + off[2]};
+        const int last = n_frames % chunk_frames;
+        rc = validate_launch(ctx, dpl, dpitch, dfs, chunk_frames);
+        if (rc == VCA_OK && last) rc = validate_launch(ctx, dpl, dpitch, dfs, last);
+        if (rc) return rc;
+    }
     int emitted = 0;
     int k = 0;
     bool used[2] = {false, false};
@@ -497,7 +528,12 @@ int vca_analyze_host(vca_ctx *ctx, const void *const host_planes[3], const int64
         void *scr = static_cast<uint8_t *>(ctx->h_scratch) + (size_t)b * ctx->h_scratch_bytes;
         if (m - halo > 0 || halo) {
             rc = launch_analysis(ctx, dpl, dpitch, dfstride, m, halo, scr, ctx->d_rec + emitted, ctx->s_comp, nullptr);
-            if (rc) return rc;
+            if (rc) {
+                // unreachable for argument errors (every chunk geometry was validated above);
+                // a CUDA error has poisoned the context already
+                ctx->poisoned = true;
+                return rc == VCA_ERR_CUDA ? rc : VCA_ERR_CUDA;
+            }
         }
         emitted += m - halo;
         VCA_CK(ctx, cudaEventRecord(ctx->ev_done[b], ctx->s_comp));
@@ -558,6 +594,7 @@ int vca_debug_dump(vca_ctx *ctx, const void *const planes[3], const int64_t pitc
     if (rc) return rc;
     DumpPtrs dp;
     memset(&dp, 0, sizeof(dp));
+    dp.on = 1;
     void *scratch = nullptr;
     rc = VCA_OK;
     cudaError_t e = cudaMalloc(&scratch, scratch_bytes(ctx, 1));
@@ -590,6 +627,51 @@ int vca_debug_dump(vca_ctx *ctx, const void *const planes[3], const int64_t pitc
     cudaFree(scratch);
     if (rc) return rc;
     return fail_cuda(ctx, e);
+}
+
+int vca_debug_analyze(vca_ctx *ctx, const void *const planes[3], const int64_t pitch_bytes[3],
+                      const int64_t frame_stride_bytes[3], int n_frames, int n_halo, void *scratch,
+                      size_t scratch_bytes_, vca_features *out_dev, int64_t *const chk_dev[3],
+                      int64_t *const sumx_dev[3], double *const H_dev[3], void *stream)
+{
+    if (!ctx) return VCA_ERR_INVALID_ARG;
+    if (ctx->poisoned) return VCA_ERR_CUDA;
+    if (n_halo < 0 || n_halo > 1 || n_frames < 1 + n_halo || !out_dev || !scratch) return VCA_ERR_INVALID_ARG;
+    int rc = check_planes(ctx, planes, pitch_bytes, frame_stride_bytes, n_frames);
+    if (rc) return rc;
+    if (((uintptr_t)scratch & 7) || scratch_bytes_ < scratch_bytes(ctx, n_frames)) return VCA_ERR_SCRATCH;
+    rc = validate_launch(ctx, planes, pitch_bytes, frame_stride_bytes, n_frames);
+    if (rc) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DumpPtrs dp;
+    memset(&dp, 0, sizeof(dp));
+    dp.on = 1;
+    for (int p = 0; p < 3; ++p) {
+        dp.chk[p] = chk_dev ? reinterpret_cast<unsigned long long *>(chk_dev[p]) : nullptr;
+        dp.sumx[p] = sumx_dev ? sumx_dev[p] : nullptr;
+        dp.H[p] = H_dev ? H_dev[p] : nullptr;
+        if (dp.chk[p])
+            VCA_CK(ctx, cudaMemsetAsync(dp.chk[p], 0, sizeof(int64_t) * (size_t)n_frames * (size_t)ctx->geo[p].count, st));
+    }
+    return launch_analysis(ctx, planes, pitch_bytes, frame_stride_bytes, n_frames, n_halo, scratch, out_dev, st, &dp);
+}
+
+int vca_debug_mutate(int plane, int64_t block, int pos, int which)
+{
+#ifdef VCA_MUTATE
+    MutSpec m;
+    m.plane = plane;
+    m.block = block;
+    m.pos = pos;
+    m.which = which;
+    return cudaMemcpyToSymbol(vca_mut, &m, sizeof(m)) == cudaSuccess ? VCA_OK : VCA_ERR_CUDA;
+#else
+    (void)plane;
+    (void)block;
+    (void)pos;
+    (void)which;
+    return VCA_ERR_INVALID_ARG;  // not a VCA_MUTATE build
+#endif
 }
 
 void vca_destroy(vca_ctx *ctx)

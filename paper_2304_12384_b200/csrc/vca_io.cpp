@@ -153,13 +153,16 @@ int read_positional(vca_reader *r, int n, void *const planes[3], const int64_t p
 {
     const int fd = fileno(r->f);
     const vca_stream_info &in = r->info;
-    std::atomic<int> bad{n};
-    std::atomic<int> code{VCA_OK};
+    // (frame index, status) of the first failing frame, packed into one word so that the
+    // pair is updated atomically: index in the high 32 bits, status (as uint32) in the low 32;
+    // an atomic min on the packed word keeps the lowest index together with its own status
+    const uint64_t none = (uint64_t)(uint32_t)n << 32;
+    std::atomic<uint64_t> first{none};
     auto fail = [&](int t, int rc) {
-        int cur = bad.load();
-        while (t < cur && !bad.compare_exchange_weak(cur, t)) {
+        const uint64_t mine = ((uint64_t)(uint32_t)t << 32) | (uint32_t)rc;
+        uint64_t cur = first.load();
+        while (mine < cur && !first.compare_exchange_weak(cur, mine)) {
         }
-        if (bad.load() == t) code.store(rc);
     };
     static const int kThreads = [] {
         const char *e = getenv("VCA_READ_THREADS");
@@ -207,8 +210,9 @@ int read_positional(vca_reader *r, int n, void *const planes[3], const int64_t p
     for (int k = 1; k < T; ++k) pool[k - 1] = std::thread(work, k);
     work(0);
     for (int k = 1; k < T; ++k) pool[k - 1].join();
-    *first_bad = bad.load();
-    return code.load();
+    const uint64_t f = first.load();
+    *first_bad = (int)(f >> 32);
+    return f == none ? VCA_OK : (int)(uint32_t)(f & 0xFFFFFFFFu);
 }
 
 }  // namespace

@@ -32,8 +32,8 @@ FEATURES = ("E_Y", "h", "L_Y", "E_U", "L_U", "E_V", "L_V")
 
 # every symbol include/vca.h and include/vca_io.h declare
 EXPORTS = ("vca_create", "vca_get_info", "vca_scratch_bytes", "vca_analyze", "vca_analyze_host", "vca_reset",
-           "vca_profile_enable", "vca_profile_read", "vca_debug_dump", "vca_destroy", "vca_status_string",
-           "vca_version",
+           "vca_profile_enable", "vca_profile_read", "vca_debug_dump", "vca_debug_analyze", "vca_debug_mutate",
+           "vca_destroy", "vca_status_string", "vca_version",
            "vca_y4m_parse_header", "vca_y4m_open", "vca_raw_open", "vca_reader_read", "vca_reader_frames",
            "vca_reader_warnings", "vca_reader_close", "vca_analyze_stream", "vca_write_csv", "vca_summarize")
 
@@ -79,6 +79,8 @@ def lib():
     L.vca_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(i64)]
     L.vca_debug_dump.argtypes = [vp, P3, I3, P3, P3, P3, P3]
+    L.vca_debug_analyze.argtypes = [vp, P3, I3, I3, c_int, c_int, vp, ctypes.c_size_t, vp, P3, P3, P3, vp]
+    L.vca_debug_mutate.argtypes = [c_int, i64, c_int, c_int]
     L.vca_destroy.argtypes = [vp]
     L.vca_destroy.restype = None
     L.vca_status_string.argtypes = [c_int]
@@ -251,6 +253,33 @@ class Analyzer:
         _check(self._L.vca_profile_read(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)),
                "vca_profile_read")
         return a.value, b.value, n.value
+
+    def debug_analyze(self, Y, U, V, n_halo: int = 0, scratch=None, stream=None):
+        """TEST-ONLY: analyze() through the DUMP kernel instantiation.  Returns (records [F - n_halo, 8],
+        scratch, per plane {"chk", "sumx", "H"} device tensors [F, count[p]])."""
+        import torch
+
+        self._check_planes((Y, U, V))
+        ptrs, pitch, fstride = _plane_args((Y, U, V), True)
+        F = Y.shape[0] if Y.dim() == 3 else 1
+        dev = Y.device
+        out = torch.empty((max(F - n_halo, 0), 8), dtype=torch.float64, device=dev)
+        if scratch is None:
+            scratch = torch.empty(self.scratch_bytes(F) // 8 + 1, dtype=torch.float64, device=dev)
+        planes = []
+        for p in range(3):
+            C = self.info["count"][p]
+            planes.append({"chk": torch.empty((F, C), dtype=torch.int64, device=dev),
+                           "sumx": torch.empty((F, C), dtype=torch.int64, device=dev),
+                           "H": torch.empty((F, C), dtype=torch.float64, device=dev)})
+        P3 = ctypes.c_void_p * 3
+        st = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+        _check(self._L.vca_debug_analyze(self._h, ptrs, pitch, fstride, F, n_halo, scratch.data_ptr(),
+                                         scratch.numel() * scratch.element_size(), out.data_ptr(),
+                                         P3(*[d["chk"].data_ptr() for d in planes]),
+                                         P3(*[d["sumx"].data_ptr() for d in planes]),
+                                         P3(*[d["H"].data_ptr() for d in planes]), st), "vca_debug_analyze")
+        return out, scratch, planes
 
     def debug_dump(self, Y, U, V):
         """TEST-ONLY: coefficients / sums / H / L of every block of one frame (device planes)."""

@@ -23,7 +23,7 @@ def run(*args, timeout=900):
 
 @pytest.mark.gpu
 def test_bench_line_contract():
-    d = run("--steps", "3", "--warmup", "3", "--frames", "32", "--e2e-frames", "16")
+    d = run("--steps", "3", "--warmup", "3", "--frames", "32", "--e2e-frames", "16", "--no-config5")
     for k in KEYS:
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["higher_is_better"] is True

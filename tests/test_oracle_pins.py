@@ -443,3 +443,44 @@ def test_first_frame_h_zero_and_nonneg(oracle_mod):
     for f in ("E_Y", "h", "L_Y", "E_U", "L_U", "E_V", "L_V"):
         assert np.all(rec[f] >= 0)
     assert np.all(rec["h"][1:] > 0)
+
+
+# --------------------------------------------------------------------- per-block integer checks
+
+@pytest.mark.parametrize("W,H,bd,w,lp", [(40, 24, 8, 8, False), (36, 20, 10, 16, True), (24, 16, 8, 4, False),
+                                         (70, 34, 8, 32, False), (72, 36, 10, 32, True)])
+def test_block_checks_brute_force(oracle_mod, W, H, bd, w, lp):
+    """The oracle's per-block test outputs (SURVEY 8(c) "Whole pipeline": AC checksum
+    sum_{(i,j)!=(0,0)} C_ij (i n + j + 1), sample sum, H) against an independent computation:
+    numpy.pad(edge) blocks, reshape-sum low-pass, exact object-integer T X T^T with the basis
+    rebuilt from scipy's orthonormal DCT-II (rint(64 sqrt(n) Phi)), fsum H -- on 2 frames of
+    ragged geometry (partial last block row and column)."""
+    rng = np.random.default_rng(W * H + bd + w)
+    hi = (1 << bd) - 1
+    dt = np.uint8 if bd == 8 else np.uint16
+    F = 2
+    Y = rng.integers(0, hi + 1, size=(F, H, W)).astype(dt)
+    U = rng.integers(0, hi + 1, size=(F, H // 2, W // 2)).astype(dt)
+    V = rng.integers(0, hi + 1, size=(F, H // 2, W // 2)).astype(dt)
+    _, checks = oracle_mod.analyze(Y, U, V, bd, w, lp, want_checks=True)
+    wc = max(4, w // 2)
+    for p, (plane, wp) in enumerate(((Y, w), (U, wc), (V, wc))):
+        n = wp // 2 if lp else wp
+        T = np.rint(64.0 * math.sqrt(n) * ortho_basis(n)).astype(np.int64).astype(object)
+        rows, cols = -(-plane.shape[1] // wp), -(-plane.shape[2] // wp)
+        for t in range(F):
+            padded = np.pad(plane[t].astype(np.int64), ((0, rows * wp - plane.shape[1]), (0, cols * wp - plane.shape[2])),
+                            mode="edge")
+            k = 0
+            for r in range(rows):
+                for c in range(cols):
+                    X = padded[r * wp:(r + 1) * wp, c * wp:(c + 1) * wp]
+                    if lp:
+                        X = (X.reshape(n, 2, n, 2).sum(axis=(1, 3)) + 2) // 4
+                    Cm = T.dot(X.astype(object)).dot(T.T)
+                    chk = sum(int(Cm[i, j]) * (i * n + j + 1) for i in range(n) for j in range(n) if (i, j) != (0, 0))
+                    assert checks[p]["chk"][t, k] == chk, (p, t, r, c)
+                    assert checks[p]["sumx"][t, k] == int(X.sum())
+                    assert checks[p]["H"][t, k] == pytest.approx(brute_H(Cm.tolist(), n), rel=1e-13, abs=1e-300)
+                    k += 1
+            assert k == checks[p]["chk"].shape[1]

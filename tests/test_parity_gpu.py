@@ -1,7 +1,9 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
 same seeded bytes.  Bar (BASELINE.json north star; R-11): integer DCT
-coefficients and DC sums bit-exact; per-frame features within 1e-6 relative,
-an exact 0 reproduced as exactly 0."""
+coefficients, DC sums and per-block AC checksums bit-exact; per-frame features
+within 1e-6 relative, an exact 0 reproduced as exactly 0; the production kernel
+instantiation bit-identical to the DUMP instantiation that exposes the integers
+(see tests/parity_util.py)."""
 import math
 
 import numpy as np
@@ -10,27 +12,9 @@ import torch
 
 import oracle
 from paper_2304_12384_b200 import Analyzer, records_to_numpy, synth
+from parity_util import FEATS, RTOL, Pair, assert_checks, assert_records, oracle_checks, planes_cuda  # noqa: F401
 
 pytestmark = pytest.mark.gpu
-
-RTOL = 1e-6
-FEATS = ("E_Y", "h", "L_Y", "E_U", "L_U", "E_V", "L_V")
-
-
-def assert_records(gpu, ref, rtol=RTOL):
-    assert len(gpu) == len(ref)
-    assert np.array_equal(gpu["poc"], ref["poc"])
-    for f in FEATS:
-        g, r = gpu[f], ref[f]
-        zero = r == 0.0
-        assert np.all(g[zero] == 0.0), f
-        rel = np.abs(g[~zero] - r[~zero]) / np.abs(r[~zero])
-        assert rel.size == 0 or rel.max() <= rtol, (f, float(rel.max()))
-
-
-def planes_cuda(Y, U, V):
-    """Device copies with 16-byte-aligned row pitch (libvca contract)."""
-    return synth.with_pitch(tuple(p.cuda() for p in (Y, U, V)))
 
 
 def run_both(Y, U, V, bd, w, lp, n_halo=0):
@@ -103,27 +87,35 @@ CASES_STRIPS = [
 
 @pytest.mark.parametrize("name,W,H,bd,w,lp", CASES + CASES_STRIPS, ids=[c[0] for c in CASES + CASES_STRIPS])
 def test_parity_small(name, W, H, bd, w, lp):
+    """Records against the oracle, the production instantiation against the DUMP one bit for
+    bit, every block's integer checks of every frame, every coefficient of frame 1."""
     F = 4
     Y, U, V = synth.g_frames(17, W, H, F, bd)
     g, r, a = run_both(Y, U, V, bd, w, lp)
     assert_records(g, r)
+    pair = Pair(W, H, bd, w, lp)
+    rec, hy, ch = pair.analyze(*planes_cuda(Y, U, V))
+    ro, rhy, rch = oracle_checks(Y, U, V, bd, w, lp)
+    assert rec.tobytes() == g.tobytes()
+    assert_records(rec, ro, rtol=1e-12)
+    assert_checks(ch, rch)
     check_dump(a, Y, U, V, bd, w, lp, frame=1)
 
 
 def test_parity_config1_cif_all_frames():
     """Config 1 whole (16 CIF frames, one call): records at 1e-6 and 1e-12, every block's H_Y,
-    and every coefficient of every fifth frame."""
+    production == DUMP instantiation bit for bit, every block's integer checks, and every
+    coefficient of every frame (SURVEY 8(c) "Whole pipeline")."""
     Y, U, V = synth.config_frames(1)
-    a = Analyzer(352, 288, 8, 32, False)
-    scratch = torch.empty(a.scratch_bytes(16) // 8 + 1, dtype=torch.float64, device="cuda")
-    g = records_to_numpy(a.analyze(*planes_cuda(Y, U, V), scratch=scratch))
-    r, rHY = oracle.analyze(*synth.as_numpy_planes(Y, U, V), 8, 32, False, want_HY=True)
+    pair = Pair(352, 288, 8, 32, False)
+    g, HY, ch = pair.analyze(*planes_cuda(Y, U, V))
+    r, rHY, rch = oracle_checks(Y, U, V, 8, 32, False)
     assert_records(g, r)
     assert_records(g, r, rtol=1e-12)
-    HY = scratch[:rHY.size].view(rHY.shape).cpu().numpy()
     assert np.all(np.abs(HY - rHY) <= 1e-12 * np.maximum(rHY, 1e-300))
-    for t in range(0, 16, 5):
-        check_dump(a, Y, U, V, 8, 32, False, frame=t)
+    assert_checks(ch, rch)
+    for t in range(16):
+        check_dump(pair.prod, Y, U, V, 8, 32, False, frame=t)
 
 
 def test_extreme_values():
@@ -231,39 +223,83 @@ def test_profile_counters():
 @pytest.mark.parametrize("cfg", (2, 3, 4))
 def test_parity_full_size_all_frames(cfg):
     """Full BASELINE.json geometry and batch, analysed in one call (the launch configuration
-    bench.py times); every record and every block's luma energy H_Y against the oracle (chunks
-    behind a halo frame for h), every feature finite and non-negative, and the coefficient dump
-    of the last frame."""
+    bench.py times): the production instantiation bit-identical to the DUMP instantiation
+    (records and every block's H_Y), and against the oracle every record, every block's H_Y and
+    the exact integer checks (AC checksum, sample sum) of every block of every plane of every
+    frame (chunks behind a one-frame halo for h), every feature finite and non-negative, and
+    the coefficient dump of the last frame."""
     c = synth.CONFIGS[cfg]
     F = c.n_frames            # the whole BASELINE.json batch in one call, as bench.py times it
     Y, U, V = synth.config_frames(cfg, device="cuda", n_frames=F)
-    a = Analyzer(c.width, c.height, c.bit_depth, c.block_size, c.lowpass)
-    scratch = torch.empty(a.scratch_bytes(F) // 8 + 1, dtype=torch.float64, device="cuda")
-    g = records_to_numpy(a.analyze(Y, U, V, scratch=scratch))
-    CY = a.info["rows"][0] * a.info["cols"][0]
-    HY = scratch[:F * CY].view(F, CY).cpu().numpy()   # per-block luma H of every frame (vca.h)
+    pair = Pair(c.width, c.height, c.bit_depth, c.block_size, c.lowpass)
+    g, HY, ch = pair.analyze(Y, U, V)
     assert len(g) == F and np.array_equal(g["poc"], np.arange(F))
     for f in FEATS:            # properties of every frame: finite, non-negative
         assert np.all(np.isfinite(g[f])) and np.all(g[f] >= 0.0), f
-    # every frame against the oracle, in host-sized chunks (each behind a one-frame halo for h),
-    # and every block's H_Y (a wrong coefficient moves H by >= w_min / (4096 n), far above
-    # the 1e-12 relative bar of two FP64 summation orders)
     step = 40
     for s in range(0, F, step):
         e = min(F, s + step)
         h0 = 1 if s > 0 else 0
-        npl = synth.as_numpy_planes(Y[s - h0:e], U[s - h0:e], V[s - h0:e])
-        r, rHY = oracle.analyze(*npl, c.bit_depth, c.block_size, c.lowpass, n_halo=h0, first_poc=s,
-                                want_HY=True)
+        r, rHY, rch = oracle_checks(Y[s - h0:e], U[s - h0:e], V[s - h0:e], c.bit_depth, c.block_size, c.lowpass,
+                                    n_halo=h0, first_poc=s)
         assert_records(g[s:e], r)
-        # and far inside it: the two sides differ only in FP64 summation order (measured
-        # <= 2e-14, tests/test_parity_margins_gpu.py), while one wrong chroma coefficient would move
-        # E_U or E_V by ~1e-10 relative -- invisible at 1e-6, caught here
+        # the sides differ only in FP64 summation order (<= 2e-14 measured,
+        # tests/test_parity_margins_gpu.py), so 1e-12 also holds.  It does NOT pin single
+        # chroma coefficients: one wrong config-4 chroma coefficient moves E_U or E_V by only
+        # ~3e-13..8e-13 relative (w / (4096 n) / (C n^2) against E ~ 50); the per-block
+        # integer checks below are what pin every coefficient.
         assert_records(g[s:e], r, rtol=1e-12)
         want = rHY[h0:]
         assert np.all(np.abs(HY[s:e] - want) <= 1e-12 * np.maximum(want, 1e-300)), s
+        assert_checks(ch, [{k: v[h0:] for k, v in d.items()} for d in rch], frames=slice(s, e))
     Yc, Uc, Vc = (p[F - 1:F].cpu() for p in (Y, U, V))
-    check_dump(a, Yc, Uc, Vc, c.bit_depth, c.block_size, c.lowpass, frame=0)
+    check_dump(pair.prod, Yc, Uc, Vc, c.bit_depth, c.block_size, c.lowpass, frame=0)
+
+
+@pytest.mark.slow
+def test_parity_config5_all_frames():
+    """Config 5 whole: 4800 UHD frames (8 segments G(10..17)) analysed as one sequence, segment
+    by segment on one context pair (the carried H_Y crosses every segment cut), production ==
+    DUMP bit for bit, every record, H_Y and per-block integer check of every frame against the
+    oracle (which gets the previous segment's H_Y as prev_HY), and GPU-count invariance: at each
+    of the 7 segment boundaries -- every rank start of the 2-, 4- and 8-GPU splits
+    (shard.plan) -- a fresh context behind a one-frame halo gives the same records bit for bit."""
+    from paper_2304_12384_b200 import shard
+
+    c = synth.CONFIGS[5]
+    S = synth.SEGMENT_FRAMES
+    starts = sorted({shard.plan(c.n_frames, wd, r).first_poc for wd in (2, 4, 8) for r in range(wd)} - {0})
+    assert starts == [S * k for k in range(1, 8)]
+    pair = Pair(c.width, c.height, 8, c.block_size, c.lowpass)
+    prev_HY = None
+    prev_last = None
+    for seg in range(c.n_frames // S):
+        Y, U, V = synth.config_frames(5, device="cuda", n_frames=S, first_t=seg * S)
+        g, HY, ch = pair.analyze(Y, U, V)
+        assert np.array_equal(g["poc"], np.arange(seg * S, (seg + 1) * S))
+        step = 60
+        for s in range(0, S, step):
+            e = min(S, s + step)
+            prev = prev_HY if s == 0 else HY[s - 1]
+            r, rHY, rch = oracle_checks(Y[s:e], U[s:e], V[s:e], 8, c.block_size, c.lowpass, first_poc=seg * S + s,
+                                        prev_HY=prev)
+            assert_records(g[s:e], r)
+            assert_records(g[s:e], r, rtol=1e-12)
+            assert np.all(np.abs(HY[s:e] - rHY) <= 1e-12 * np.maximum(rHY, 1e-300)), (seg, s)
+            assert_checks(ch, rch, frames=slice(s, e))
+        if seg > 0:
+            # a rank starting at this segment: fresh context, halo = the previous segment's last frame
+            assert g["h"][0] > 0.0            # h across the cut, not a sequence restart
+            b = Analyzer(c.width, c.height, 8, c.block_size, c.lowpass)
+            b.reset(seg * S)
+            Yh, Uh, Vh = (torch.cat([q, p]) for q, p in zip(prev_last, (Y, U, V)))
+            ranked = records_to_numpy(b.analyze(Yh, Uh, Vh, n_halo=1))
+            assert ranked.tobytes() == g.tobytes(), seg
+            del Yh, Uh, Vh, b
+        prev_HY = HY[-1].copy()
+        prev_last = tuple(p[-1:].clone() for p in (Y, U, V))
+        del Y, U, V
+        torch.cuda.empty_cache()
 
 
 @pytest.mark.slow
