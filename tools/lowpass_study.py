@@ -1,24 +1,34 @@
 #!/usr/bin/env python
-"""NEXT-2: the paper's low-pass DCT optimisation (mode m2 vs m1,
-P:118) measured on B200.
+"""NEXT-2: the paper's low-pass optimisation and the cross-resolution stability of
+E_Y, measured on B200 with the HEAD build, to SPEC's acceptance criteria 6 and 8
+(the paper: "spatially downsampled by a factor of two",
+P:118 m2 vs m1).
 
-On the same UHD 8-bit clips (config 5's segments, G(10 + s)), block 32, the
-analyzer runs with the full 32x32 DCT and with the low-pass DCT (2x2 mean, 16x16
-DCT, R-5).  Reported per clip:
+Corpus: >= 20 seeded synthetic clips -- generator G(seed) of BASELINE.json config 2 (three
+moving oriented sinusoids + noise, scene cuts), seeds 100.., rendered at 2160p and area-
+downsampled (2x2 / 4x4 box mean, rounded) to 1080p and 540p: the same content at three
+resolutions, as an encoding ladder would have it.  Stands in for the paper's unnamed UHD
+videos; nothing here is from a dataset.
 
-* throughput of each mode (device-resident frames, CUDA events around
-  vca_analyze, best of R repetitions) and the low-pass speed-up;
-* agreement of the features between the modes: Pearson correlation over frames
-  of E_Y, h and L_Y (the paper's premise: E_Y "exhibits better correlation
-  across resolutions"), and the across-clip correlation of the clip means.
-
-Writes one JSON object per clip plus a summary line to stdout.
-usage: lowpass_study.py [--clips 8] [--frames 120] [--reps 5]
+Per clip:
+  * fps of the full 32x32 DCT and of the low-pass DCT (2x2 mean + 16x16 DCT) at 2160p, same
+    device-resident frames, CUDA events around vca_analyze, best of --reps;
+  * mean E_Y at 2160p full, 2160p low-pass, 1080p and 540p (block size by the auto rule S:250:
+    32 / 16 / 8, full DCT), plus per-frame PCC of E_Y low-pass vs full.
+Summary (the acceptance numbers):
+  * speedup = fps(low-pass) / fps(full)   (criterion 8: >= 1.8)
+  * PCC over clips of mean E_Y, low-pass vs full at 2160p   (criterion 8: >= 0.90)
+  * PCC over clips of mean E_Y across resolution pairs 2160/1080, 2160/540, 1080/540
+    (criterion 6: >= 0.90; its SI comparison is out of scope -- SI/TI is the paper's comparison
+    system).
+usage: lowpass_study.py [--clips 24] [--frames 48] [--reps 5] [--out FILE]
 """
 import argparse
 import json
 import os
+import subprocess
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -45,47 +55,80 @@ def timed(a, planes, reps):
     return records_to_numpy(out), best
 
 
+def downsample(planes, f):
+    """Area (f x f box mean, rounded half to even) downsampling of uint8 planes: input rendering."""
+    res = []
+    for p in planes:
+        q = torch.nn.functional.avg_pool2d(p.float().unsqueeze(1), f).squeeze(1)
+        res.append(torch.round(q).clamp(0, 255).to(torch.uint8).contiguous())
+    return tuple(res)
+
+
 def pcc(x, y):
     x = np.asarray(x, np.float64)
     y = np.asarray(y, np.float64)
-    if x.std() == 0 or y.std() == 0:
+    if len(x) < 3 or x.std() == 0 or y.std() == 0:
         return float("nan")
     return float(np.corrcoef(x, y)[0, 1])
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--clips", type=int, default=8)
-    ap.add_argument("--frames", type=int, default=120)
+    ap.add_argument("--clips", type=int, default=24)
+    ap.add_argument("--frames", type=int, default=48)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--first-seed", type=int, default=100)
+    ap.add_argument("--out", default=None)
     args = ap.parse_args()
     W, H = 3840, 2160
-    full = Analyzer(W, H, 8, 32, False)
-    low = Analyzer(W, H, 8, 32, True)
-    means = {"full": [], "low": []}
+    an = {"full": Analyzer(W, H, 8, 32, False), "low": Analyzer(W, H, 8, 32, True),
+          "1080": Analyzer(W // 2, H // 2, 8, 0, False), "540": Analyzer(W // 4, H // 4, 8, 0, False)}
     rows = []
+    t0 = time.time()
     for s in range(args.clips):
-        planes = synth.g_frames(10 + s, W, H, args.frames, 8, 0, "cuda")
-        rf, tf = timed(full, planes, args.reps)
-        rl, tl = timed(low, planes, args.reps)
-        row = {"clip": "G(%d)" % (10 + s), "frames": args.frames,
+        seed = args.first_seed + s
+        uhd = synth.g_frames(seed, W, H, args.frames, 8, 0, "cuda")
+        rf, tf = timed(an["full"], uhd, args.reps)
+        rl, tl = timed(an["low"], uhd, args.reps)
+        r2, _ = timed(an["1080"], downsample(uhd, 2), 1)
+        r4, _ = timed(an["540"], downsample(uhd, 4), 1)
+        row = {"clip": "G(%d)" % seed, "frames": args.frames,
                "fps_full": args.frames / tf * 1e3, "fps_lowpass": args.frames / tl * 1e3, "speedup": tf / tl,
-               "pcc_E_Y": pcc(rf["E_Y"], rl["E_Y"]), "pcc_h": pcc(rf["h"][1:], rl["h"][1:]),
-               "pcc_L_Y": pcc(rf["L_Y"], rl["L_Y"]),
-               "mean_E_Y_full": float(rf["E_Y"].mean()), "mean_E_Y_lowpass": float(rl["E_Y"].mean()),
-               "ratio_E_Y_low_over_full": float(rl["E_Y"].mean() / rf["E_Y"].mean())}
+               "mean_E_Y": {"2160_full": float(rf["E_Y"].mean()), "2160_lowpass": float(rl["E_Y"].mean()),
+                            "1080": float(r2["E_Y"].mean()), "540": float(r4["E_Y"].mean())},
+               "pcc_frames_E_Y_low_vs_full": pcc(rf["E_Y"], rl["E_Y"]),
+               "block": {"1080": an["1080"].info["block"][0], "540": an["540"].info["block"][0]}}
         rows.append(row)
-        means["full"].append(row["mean_E_Y_full"])
-        means["low"].append(row["mean_E_Y_lowpass"])
         print(json.dumps(row), flush=True)
-        del planes
+        del uhd
         torch.cuda.empty_cache()
-    summ = {"summary": True, "clips": len(rows),
+    m = {k: [r["mean_E_Y"][k] for r in rows] for k in rows[0]["mean_E_Y"]}
+    try:
+        git = subprocess.run(["git", "rev-parse", "--short", "HEAD"], cwd=ROOT, capture_output=True,
+                             text=True).stdout.strip() or None
+    except Exception:
+        git = None
+    summ = {"summary": True, "clips": len(rows), "frames_per_clip": args.frames, "git": git,
+            "gpu": torch.cuda.get_device_name(0), "elapsed_s": time.time() - t0,
             "speedup_mean": float(np.mean([r["speedup"] for r in rows])),
-            "pcc_E_Y_min": float(np.min([r["pcc_E_Y"] for r in rows])),
-            "pcc_h_min": float(np.nanmin([r["pcc_h"] for r in rows])),
-            "pcc_clip_mean_E_Y": pcc(means["full"], means["low"]) if len(rows) > 2 else None}
+            "speedup_min": float(np.min([r["speedup"] for r in rows])),
+            "pcc_clip_mean_E_Y_lowpass_vs_full": pcc(m["2160_full"], m["2160_lowpass"]),
+            "pcc_clip_mean_E_Y_2160_vs_1080": pcc(m["2160_full"], m["1080"]),
+            "pcc_clip_mean_E_Y_2160_vs_540": pcc(m["2160_full"], m["540"]),
+            "pcc_clip_mean_E_Y_1080_vs_540": pcc(m["1080"], m["540"]),
+            "pcc_frames_E_Y_low_vs_full_min": float(np.nanmin([r["pcc_frames_E_Y_low_vs_full"] for r in rows])),
+            "criteria": {"speedup_ge_1.8": None, "pcc_lowpass_ge_0.90": None, "pcc_cross_res_ge_0.90": None}}
+    summ["criteria"]["speedup_ge_1.8"] = summ["speedup_min"] >= 1.8
+    summ["criteria"]["pcc_lowpass_ge_0.90"] = summ["pcc_clip_mean_E_Y_lowpass_vs_full"] >= 0.90
+    summ["criteria"]["pcc_cross_res_ge_0.90"] = min(summ["pcc_clip_mean_E_Y_2160_vs_1080"],
+                                                     summ["pcc_clip_mean_E_Y_2160_vs_540"],
+                                                     summ["pcc_clip_mean_E_Y_1080_vs_540"]) >= 0.90
     print(json.dumps(summ), flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            for r in rows:
+                fh.write(json.dumps(r) + "\n")
+            fh.write(json.dumps(summ) + "\n")
 
 
 if __name__ == "__main__":

@@ -71,6 +71,8 @@ def main():
     ap.add_argument("--frames", type=int, default=0)
     ap.add_argument("--frame-bytes", type=int, default=0)
     ap.add_argument("--workload")
+    ap.add_argument("--git", default=None, help="commit of the captured build (recorded with the traffic)")
+    ap.add_argument("--date", default=None)
     a = ap.parse_args()
     ks = raw(a.report)
     for d in ks:
@@ -93,7 +95,8 @@ def main():
                                  "ncu_traffic.json")
                 js = json.load(open(p)) if os.path.exists(p) else {}
                 js[a.workload] = {"dram_bytes_per_frame": (rd + wr) / a.frames, "read": rd, "write": wr,
-                                  "frames": a.frames, "report": os.path.basename(a.report)}
+                                  "frames": a.frames, "report": os.path.basename(a.report), "git": a.git,
+                                  "date": a.date}
                 json.dump(js, open(p, "w"), indent=1)
         print("\nwarp stall reasons (warps per issue-active cycle):\n")
         for k, v in stalls(a.report)[:12]:
