@@ -151,7 +151,7 @@ __global__ void k_correct(const int8_t *A, const int8_t *Bt, int a_mn, int a_s8,
         uint32_t r[32];
         LD32(tm + ((uint32_t)(32 * warp) << 16) + c, r);
         tmem_wait_ld();
-        for (int j = 0; j < 32; ++j) D[(32 * warp + lane) * N + c + j] = (int32_t)r[j];
+        for (int j = 0; j < 32 && c + j < N; ++j) D[(32 * warp + lane) * N + c + j] = (int32_t)r[j];
     }
     fence_before();
     __syncthreads();
@@ -159,7 +159,7 @@ __global__ void k_correct(const int8_t *A, const int8_t *Bt, int a_mn, int a_s8,
 }
 
 // ---- 2. MMA issue rate
-template <int N>
+template <int N, int NACC>
 __global__ void k_mma_rate(int iters, long long *cycles)
 {
     __shared__ __align__(1024) uint8_t sA[128 * 32];
@@ -184,11 +184,11 @@ __global__ void k_mma_rate(int iters, long long *cycles)
         const uint64_t bd = sdesc(smem_u32(sB), 128, 256);
         const uint32_t id = idesc_i8(128, N, true, false, false, false);
         // warm-up
-        for (int i = 0; i < 8; ++i) mma_i8(tm + (i & 1) * N % 512, ad, bd, id, 1);
+        for (int i = 0; i < 8; ++i) mma_i8(tm + ((i % NACC) * N) % 512, ad, bd, id, 1);
         mma_commit(&bar);
         mbar_wait(&bar, 0);
         const long long t0 = clock64();
-        for (int i = 0; i < iters; ++i) mma_i8(tm + ((i & 1) * N) % 512, ad, bd, id, 1);
+        for (int i = 0; i < iters; ++i) mma_i8(tm + ((i % NACC) * N) % 512, ad, bd, id, i >= NACC);
         mma_commit(&bar);
         mbar_wait(&bar, 1);
         const long long t1 = clock64();
@@ -200,7 +200,7 @@ __global__ void k_mma_rate(int iters, long long *cycles)
 }
 
 // ---- 3. TMEM load bandwidth: every warp loads its lane quadrant, X columns per instruction
-template <int X>
+template <int X, int DEPTH>
 __global__ void k_ld_rate(int iters, long long *cycles, uint32_t *sink)
 {
     __shared__ uint32_t tbase;
@@ -213,17 +213,22 @@ __global__ void k_ld_rate(int iters, long long *cycles, uint32_t *sink)
     uint32_t acc = 0;
     __syncthreads();
     const long long t0 = clock64();
-    for (int i = 0; i < iters; ++i) {
-        const uint32_t col = (uint32_t)((i * X + (warp >> 2) * 64) & 511);
-        uint32_t r[32];
-        if (X == 32) {
-            LD32(tm + col, r);
-        } else {
-            LD16(tm + col, r);
+    for (int i = 0; i < iters; i += DEPTH) {
+        uint32_t r[DEPTH][32];
+#pragma unroll
+        for (int d = 0; d < DEPTH; ++d) {
+            const uint32_t col = (uint32_t)(((i + d) * X + (warp >> 2) * 64) & 511);
+            if (X == 32) {
+                LD32(tm + col, r[d]);
+            } else {
+                LD16(tm + col, r[d]);
+            }
         }
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < X; ++j) acc += r[j];
+        for (int d = 0; d < DEPTH; ++d)
+#pragma unroll
+            for (int j = 0; j < X; ++j) acc += r[d][j];
     }
     __syncthreads();
     const long long t1 = clock64();
@@ -275,13 +280,13 @@ bool run_correct(int a_mn, int a_s8, int b_s8)
     return bad == 0;
 }
 
-template <int N>
+template <int N, int NACC>
 void run_mma_rate(int sms)
 {
     long long *dc;
     CK(cudaMalloc(&dc, sizeof(long long) * sms));
     const int iters = 4096;
-    k_mma_rate<N><<<sms, 128>>>(iters, dc);
+    k_mma_rate<N, NACC><<<sms, 128>>>(iters, dc);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     std::vector<long long> c(sms);
@@ -289,12 +294,12 @@ void run_mma_rate(int sms)
     double mx = 0;
     for (auto v : c) mx = v > mx ? v : mx;
     const double cyc = mx / iters;
-    printf("mma M=128 N=%3d K=32 i8: %.2f cycles/MMA per SM (%d CTAs), %.0f MACs/cycle/SM\n", N, cyc, sms,
-           128.0 * N * 32 / cyc);
+    printf("mma M=128 N=%3d K=32 i8, %d accumulators: %.2f cycles/MMA per SM (%d CTAs), %.0f MACs/cycle/SM\n", N,
+           NACC, cyc, sms, 128.0 * N * 32 / cyc);
     cudaFree(dc);
 }
 
-template <int X>
+template <int X, int DEPTH>
 void run_ld_rate(int warps, int sms)
 {
     long long *dc;
@@ -302,7 +307,7 @@ void run_ld_rate(int warps, int sms)
     CK(cudaMalloc(&dc, sizeof(long long) * sms));
     CK(cudaMalloc(&sink, 4 * 1024));
     const int iters = 2048;
-    k_ld_rate<X><<<sms, 32 * warps>>>(iters, dc, sink);
+    k_ld_rate<X, DEPTH><<<sms, 32 * warps>>>(iters, dc, sink);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     std::vector<long long> c(sms);
@@ -310,8 +315,8 @@ void run_ld_rate(int warps, int sms)
     double mx = 0;
     for (auto v : c) mx = v > mx ? v : mx;
     const double bytes = (double)warps * iters * 32 * X * 4;
-    printf("tcgen05.ld 32x32b.x%d, %2d warps/SM: %.1f bytes/cycle/SM (%.1f cycles per warp-load)\n", X, warps,
-           bytes / mx, mx / iters);
+    printf("tcgen05.ld 32x32b.x%d, %d in flight, %2d warps/SM: %.1f bytes/cycle/SM (%.1f cycles per warp-load)\n", X,
+           DEPTH, warps, bytes / mx, mx / iters);
     cudaFree(dc);
     cudaFree(sink);
 }
@@ -328,14 +333,19 @@ int main()
     ok &= run_correct<16>(0, 0, 1);
     ok &= run_correct<32>(1, 1, 1);
     printf("descriptor correctness: %s\n", ok ? "all ok" : "FAILURES");
-    run_mma_rate<32>(sms);
-    run_mma_rate<64>(sms);
-    run_mma_rate<128>(sms);
-    run_mma_rate<256>(sms);
-    run_mma_rate<32>(1);
+    run_mma_rate<32, 2>(sms);
+    run_mma_rate<32, 8>(sms);
+    run_mma_rate<32, 16>(sms);
+    run_mma_rate<64, 2>(sms);
+    run_mma_rate<64, 8>(sms);
+    run_mma_rate<128, 2>(sms);
+    run_mma_rate<128, 4>(sms);
+    run_mma_rate<256, 2>(sms);
     for (int w : {4, 8, 16}) {
-        run_ld_rate<32>(w, sms);
-        run_ld_rate<16>(w, sms);
+        run_ld_rate<32, 1>(w, sms);
+        run_ld_rate<32, 2>(w, sms);
+        run_ld_rate<32, 4>(w, sms);
+        run_ld_rate<16, 4>(w, sms);
     }
     return 0;
 }
