@@ -94,6 +94,20 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// L2 prefetch of a box a few strips ahead of the ring (VCA_L2PF strips; 0 = off): the later
+// TMA load of the same box then hits L2 instead of HBM.  A/B (profiles/r02/ab_l2_prefetch_reverted.log,
+// 1 / 2 / 4 strips ahead): config 3 -4 %, config 4 -2..-4 %, config 2 -2 % -- off.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int x, int y, int z)
+{
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+#ifndef VCA_L2PF
+#define VCA_L2PF 0
+#endif
+
 #define VCA_MMA_ASM asm volatile  // A/B: non-volatile (reorderable) MMA asm was neutral
 // D = A(s8) . B(u8) + C, m16n8k16
 __device__ __forceinline__ void mma16_su(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t b)
@@ -1465,9 +1479,33 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
             uint32_t st = 0, phase = 0;
             bool first_pass = true;
+            // prefetch cursor VCA_L2PF strips ahead of the load cursor (same item sequence)
+            int pit = vblk, ps = 0;
+            if (VCA_L2PF > 0) {
+                for (int k = 0; k < VCA_L2PF && pit < items; ++k)
+                    if (++ps == strips) {
+                        ps = 0;
+                        pit += vgrid;
+                    }
+            }
             for (int it = vblk; it < items; it += vgrid) {
                 const int f = it / rows, r = it - f * rows;
                 for (int s = 0; s < strips; ++s) {
+                    if (VCA_L2PF > 0 && pit < items) {
+                        const int pf = pit / rows, pr = pit - pf * rows;
+#pragma unroll
+                        for (int b = 0; b < F::NBOX_Y; ++b)
+                            tma_prefetch_3d(&tmY, (ps * F::UNITS + b * F::UPB_Y) * W, pr * W, pf);
+#pragma unroll
+                        for (int b = 0; b < F::NBOX_C; ++b) {
+                            tma_prefetch_3d(&tmU, (ps * F::UNITS + b * F::UPB_C) * WC, pr * WC, pf);
+                            tma_prefetch_3d(&tmV, (ps * F::UNITS + b * F::UPB_C) * WC, pr * WC, pf);
+                        }
+                        if (++ps == strips) {
+                            ps = 0;
+                            pit += vgrid;
+                        }
+                    }
                     if (!first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
                     uint8_t *base = smem + st * F::STAGE;
 #ifdef VCA_NULL_MEMORY

@@ -86,3 +86,17 @@ def test_plan():
     assert cov == list(range(10))
     with pytest.raises(ValueError):
         shard.plan(2, 3, 0)
+
+
+def test_config5_strong_scaling_plan():
+    """bench.py at N > 1 (config 5, strong scaling): 4800 frames in contiguous ranges of 4800 / N,
+    every rank after the first behind a one-frame halo, every rank start on a 600-frame segment
+    boundary for N = 2, 4, 8 (so each rank's halo is the previous segment's last frame)."""
+    for world in (1, 2, 4, 8):
+        plans = [shard.plan(4800, world, r) for r in range(world)]
+        assert sum(p.count for p in plans) == 4800
+        assert [p.first_poc for p in plans] == [r * 4800 // world for r in range(world)]
+        for r, p in enumerate(plans):
+            assert p.count == 4800 // world and p.n_halo == (1 if r else 0)
+            assert p.first_frame == p.first_poc - p.n_halo and p.n_frames == p.count + p.n_halo
+            assert p.first_poc % 600 == 0
