@@ -854,7 +854,28 @@ struct FusedArgs {
     const int8_t *T_all;
     Scratch s;
     DumpPtrs dump;
+    // dynamic item scheduling (VCA_DYN): a context-owned ticket counter that is never reset;
+    // this launch owns tickets [ticket_base, ticket_base + items + groups)
+    unsigned long long *ticket;
+    unsigned long long ticket_base;
 };
+
+// Work distribution over the consumer groups.  0: static round robin (item it goes to virtual
+// CTA it mod (grid x groups)); 1: dynamic -- each group's producer takes the next item from a
+// global ticket counter and passes its index to the consumers in a per-stage header word, so
+// groups on faster SMs take more items and the launch ends when the work does, not when the
+// slowest SM's fixed share does.  Results do not depend on the assignment (every item's sums
+// are computed in a fixed order by whichever group takes it).
+#ifndef VCA_DYN
+#define VCA_DYN 0
+#endif
+
+// A ragged last strip (fewer whole units than a full strip: config 3's 120 block columns are
+// 7.5 strips of 16) runs each warp's first two whole units as one 2-unit group instead of two
+// single units (A/B: VCA_RAGGED2 0 / 1)
+#ifndef VCA_RAGGED2
+#define VCA_RAGGED2 1
+#endif
 
 template <class F>
 struct UnitCtx {
@@ -1409,7 +1430,8 @@ constexpr int kConsumers = 4;
 
 template <class F>
 struct Lay {  // shared-memory layout (offsets from the 1024-aligned base)
-    static constexpr int GRP = (F::STAGES * F::STAGE + 2 * F::STAGES * 8 + 1023) / 1024 * 1024;  // ring + bars
+    // ring + full/empty barriers + per-stage header words (VCA_DYN item index)
+    static constexpr int GRP = (F::STAGES * F::STAGE + 2 * F::STAGES * 8 + F::STAGES * 4 + 1023) / 1024 * 1024;
     static constexpr int WTAB_OFF = F::GV * GRP;
     static constexpr int STASH_OFF = WTAB_OFF + (F::WTAB ? 32 * 32 * 8 : 0);
     static constexpr int WSM_OFF = STASH_OFF + 4 * F::GV * F::STASH;
@@ -1479,6 +1501,43 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmV)) : "memory");
             uint32_t st = 0, phase = 0;
             bool first_pass = true;
+#if VCA_DYN
+            int *hdr = reinterpret_cast<int *>(empty + F::STAGES);
+            for (;;) {
+                const unsigned long long tk = atomicAdd(a.ticket, 1ull) - a.ticket_base;
+                const int it = tk < (unsigned long long)items ? (int)tk : -1;
+                if (!first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
+                hdr[st] = it;  // published by the arrive below (release), read after the consumers' wait
+                if (it < 0) {
+                    mbar_arrive(smem_u32(&full[st]));  // end marker: a stage with no data
+                    break;
+                }
+                const int f = it / rows, r = it - f * rows;
+                for (int s = 0; s < strips; ++s) {
+                    if (s > 0 && !first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
+                    uint8_t *base = smem + st * F::STAGE;
+                    mbar_expect_tx(&full[st], F::TX);
+#pragma unroll
+                    for (int b = 0; b < F::NBOX_Y; ++b)
+                        tma_load_3d(base + b * F::BOXB_Y, &tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * W,
+                                    r * W, f, policy);
+#pragma unroll
+                    for (int b = 0; b < F::NBOX_C; ++b) {
+                        tma_load_3d(base + F::ST_Y + b * F::BOXB_C, &tmU, &full[st],
+                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                        tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
+                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                    }
+                    if (++st == F::STAGES) {
+                        st = 0;
+                        phase ^= 1;
+                        first_pass = false;
+                    }
+                }
+            }
+            (void)vblk;
+            (void)vgrid;
+#else
             // prefetch cursor VCA_L2PF strips ahead of the load cursor (same item sequence)
             int pit = vblk, ps = 0;
             if (VCA_L2PF > 0) {
@@ -1539,6 +1598,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     }
                 }
             }
+#endif
         }
         return;
     }
@@ -1623,7 +1683,15 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
     const int s_fast = cols_whole > last_c ? (cols_whole - last_c - 1) / F::UNITS + 1 : 0;
 
     uint32_t st = 0, phase = 0;
+#if VCA_DYN
+    const uint32_t hdr0 = smem_off(empty + F::STAGES);
+    for (;;) {
+        mbar_wait(full0 + 8 * st, phase);  // the item's first stage, or the end marker
+        const int it = lds<int>(hdr0 + 4 * st);
+        if (it < 0) break;
+#else
     for (int it = vblk; it < items; it += vgrid) {
+#endif
         const int f = it / rows, r = it - f * rows;
         const int hvY = min(W, a.height[0] - r * W), hvC = min(WC, a.height[1] - r * WC);
         double hu = 0.0, hv = 0.0;                          // per-lane U/V texture partials (fixed order)
@@ -1644,7 +1712,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
         for (int s0 = 0; s0 < strips; s0 += SPCW) {
         const int s1 = min(strips, s0 + SPCW);
         for (int s = s0; s < s1; ++s) {
-            mbar_wait(full0 + 8 * st, phase);
+            if (!VCA_DYN || s > 0) mbar_wait(full0 + 8 * st, phase);
             // this warp's units of strip s: c_n = s*UNITS + u + 4n, n < NU, in ascending order;
             // unit m = s*NU + n of the item goes to stash slot m & 31
             const uint32_t base = smem0 + st * F::STAGE;
@@ -1715,11 +1783,36 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     if (lane == 0) sts<uint4>(sxs + (sl0 + n) * 16, make_uint4(o[n].dcY, o[n].dcU, o[n].dcV, 0u));
                 }
             } else {
-                // ragged strip end or a partial last block column: one unit at a time
+                // ragged strip end or a partial last block column: whole units 0 and 1 of this
+                // warp (if any) as one 2-unit group, the rest one unit at a time
+                int n0 = 0;
+                if (VCA_RAGGED2 && NU >= 4 && c0 + 4 < cols_whole) {
+                    uint32_t bY[2], bU[2];
+                    int uY[2], uC[2];
+                    int64_t kk[2];
+#pragma unroll
+                    for (int n = 0; n < 2; ++n) {
+                        bY[n] = base + offY[n];
+                        bU[n] = base + offU[n];
+                        uY[n] = ubYc[n];
+                        uC[n] = ubCc[n];
+                        kk[n] = fCY + (int64_t)r * cols + c0 + 4 * n;
+                    }
+                    UnitOut o2[2];
+                    process_units<F, false, DUMP, 2>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o2, hu, hv, ca);
+                    const uint32_t sl0 = (uint32_t)((s % F::SPF) * NU);
+#pragma unroll
+                    for (int n = 0; n < 2; ++n) {
+                        if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, o2[n].hY);
+                        if (lane == 0)
+                            sts<uint4>(sxs + (sl0 + n) * 16, make_uint4(o2[n].dcY, o2[n].dcU, o2[n].dcV, 0u));
+                    }
+                    n0 = 2;
+                }
 #pragma unroll
                 for (int n = 0; n < NU; ++n) {
                     const int c = c0 + 4 * n;
-                    if (c >= cols) continue;
+                    if (n < n0 || c >= cols) continue;
                     const int v = u + 4 * n;
                     const uint32_t bY[1] = {base + (v / F::UPB_Y) * F::BOXB_Y};
                     const uint32_t bU[1] = {base + F::ST_Y + (v / F::UPB_C) * F::BOXB_C};
@@ -1882,7 +1975,8 @@ inline cudaError_t fused_prepare(int bd, int lowpass, int w)
 
 template <int W, int BD, int LP>
 inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const double *Wt, const Scratch &s,
-                      const DumpPtrs &dp, int sm_count, cudaStream_t st)
+                      const DumpPtrs &dp, int sm_count, cudaStream_t st, unsigned long long *ticket,
+                      unsigned long long *ticket_base)
 {
     using F = Fam<W, BD, LP>;
     CUtensorMap mY, mU, mV;
@@ -1901,6 +1995,8 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     a.T_all = T;
     a.s = s;
     a.dump = dp;
+    a.ticket = ticket;
+    a.ticket_base = ticket_base ? *ticket_base : 0;
     const bool dump = dp.on != 0;
     auto kern = dump ? fused_kernel<W, BD, LP, true> : fused_kernel<W, BD, LP, false>;
     // CTAs per SM: a property of the kernel and the device, queried once per instantiation
@@ -1918,6 +2014,8 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     int64_t grid = (int64_t)sm_count * per_sm;
     if (grid > items) grid = items;
     kern<<<(unsigned)grid, F::THREADS, Lay<F>::SMEM, st>>>(mY, mU, mV, a);
+    // every group takes exactly one ticket past the last item: the next launch starts after them
+    if (ticket_base) *ticket_base += (unsigned long long)items + (unsigned long long)grid * F::GV;
     return 0;
 }
 
@@ -1944,23 +2042,24 @@ inline bool fused_check(const Planes3 &pl, int n_frames, int bd, int lowpass)
 // Returns 0 on launch, -1 on a CUDA launch failure (see cudaGetLastError), -2 if a
 // tensor map could not be encoded.
 inline int launch_fused(const Planes3 &pl, int n_frames, int bd, int lowpass, const int8_t *T, const double *Wt,
-                        const Scratch &s, const DumpPtrs &dp, int sm_count, cudaStream_t st)
+                        const Scratch &s, const DumpPtrs &dp, int sm_count, cudaStream_t st, unsigned long long *ticket,
+                        unsigned long long *ticket_base)
 {
     const int w = pl.p[0].w;
     if (w == 32 && lowpass)
-        return bd == 8 ? launch_one<32, 8, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st)
-                       : launch_one<32, 10, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+        return bd == 8 ? launch_one<32, 8, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base)
+                       : launch_one<32, 10, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base);
     if (w == 32)
-        return bd == 8 ? launch_one<32, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
-                       : launch_one<32, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+        return bd == 8 ? launch_one<32, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base)
+                       : launch_one<32, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base);
     if (w == 16 && lowpass)
-        return bd == 8 ? launch_one<16, 8, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st)
-                       : launch_one<16, 10, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+        return bd == 8 ? launch_one<16, 8, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base)
+                       : launch_one<16, 10, 1>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base);
     if (w == 8)
-        return bd == 8 ? launch_one<8, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
-                       : launch_one<8, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
-    return bd == 8 ? launch_one<16, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st)
-                   : launch_one<16, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st);
+        return bd == 8 ? launch_one<8, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base)
+                       : launch_one<8, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base);
+    return bd == 8 ? launch_one<16, 8, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base)
+                   : launch_one<16, 10, 0>(pl, n_frames, T, Wt, s, dp, sm_count, st, ticket, ticket_base);
 }
 
 }  // namespace vca

@@ -39,6 +39,8 @@ struct vca_ctx {
     int8_t *d_T = nullptr;     // basis tables, all sizes
     double *d_W = nullptr;     // scaled weight tables, all sizes
     double *d_prevHY = nullptr;  // two buffers of C_Y doubles: [cur_prev] holds the carried H_Y
+    unsigned long long *d_ticket = nullptr;  // dynamic item scheduling (VCA_DYN): never reset
+    unsigned long long ticket_base = 0;      // first ticket of the next launch
     int cur_prev = 0;
     bool prev_valid = false;
     int64_t next_poc = 0;
@@ -215,7 +217,8 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
         VCA_CK(ctx, cudaEventRecord(ev.e[0], st));
     }
     if (ctx->path == VCA_PATH_FUSED_MMA) {
-        const int rc = launch_fused(pl, n_frames, ctx->bd, ctx->lowpass, ctx->d_T, ctx->d_W, s, dp, ctx->sm_count, st);
+        const int rc = launch_fused(pl, n_frames, ctx->bd, ctx->lowpass, ctx->d_T, ctx->d_W, s, dp, ctx->sm_count, st,
+                                    ctx->d_ticket, &ctx->ticket_base);
         if (rc == -2) return VCA_ERR_INVALID_ARG;  // tensor map not encodable for these strides
     } else {
         const int64_t tasks = (int64_t)n_frames * (ctx->geo[0].count + ctx->geo[1].count + ctx->geo[2].count);
@@ -361,6 +364,8 @@ int vca_create(int width, int height, int bit_depth, int chroma_format, int bloc
     if (e == cudaSuccess) e = cudaMalloc(&c->d_T, sizeof(hT));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_W, sizeof(hW));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_prevHY, 2 * sizeof(double) * (size_t)c->geo[0].count);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_ticket, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->d_ticket, 0, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemcpy(c->d_T, hT, sizeof(hT), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(c->d_W, hW, sizeof(hW), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && c->path == VCA_PATH_FUSED_MMA) e = fused_prepare(c->bd, c->lowpass, w);
@@ -680,6 +685,7 @@ void vca_destroy(vca_ctx *ctx)
     cudaFree(ctx->d_T);
     cudaFree(ctx->d_W);
     cudaFree(ctx->d_prevHY);
+    cudaFree(ctx->d_ticket);
     for (int b = 0; b < 2; ++b) cudaFree(ctx->stage[b]);
     cudaFree(ctx->h_scratch);
     cudaFree(ctx->d_rec);
