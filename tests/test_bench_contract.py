@@ -44,3 +44,30 @@ def test_reference_arm_contract():
     d = run("--impl", "reference", "--steps", "1", "--warmup", "3")
     assert d["impl"] == "reference" and d["unit"] == "frames/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bench_strong_scaling_gloo_functional():
+    """bench.py at N = 2 (config 5, strong scaling: 2 x 2400 frames + halo), run functionally with
+    the gloo backend and both ranks on one GPU: the gathered 4800 records are byte-identical to one
+    context over the whole sequence (--verify) and carry the same digest."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, VCA_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--steps", "1", "--warmup", "3", "--no-e2e", "--verify"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=1200, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["frames_total"] == 4800
+    assert d["config"]["frames_per_gpu"] == 2400 and len(d["per_rank"]) == 2
+    assert d["sanity"]["records"] == 4800 and d["verify"]["identical"] is True
+    assert d["verify"]["single_context_sha256"] == d["sanity"]["records_sha256"]
