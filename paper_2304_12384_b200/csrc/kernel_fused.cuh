@@ -507,6 +507,7 @@ struct LaneConst {
     int32_t zq[4];      // pass-1 init {off_g, off_g, 2^17, 2^17}, off_g = 0 for g = 0, else 2^17
     float mq[4];        // pass-2 init 0.75 (bits 0x3F400000)
     int32_t kL0, kL1, kC0, kC1;  // combine constants -0x7F400000 - r_0 off_k (luma / chroma)
+    int32_t mL0, mL1, mC0, mC1, mK;  // VCA_MIXP2 lo-plane accumulator inits -256 * 0x3F400000 - r_0 off_k
 };
 
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d)
@@ -571,6 +572,14 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
         L.kL1 = g == 0 ? K - (1 << 27) : K;
         L.kC0 = (g == 0 && t != 0) ? K - (1 << 26) : K;
         L.kC1 = g == 0 ? K - (1 << 26) : K;
+        // mixed pass 2 (VCA_MIXP2): C = E_lo + 256 bits(E_hi) - 256 * 0x3F400000 - r_0 off_k, the constant
+        // in the lo-plane IMMA's accumulator (256 * 0x3F400000 = 0x40000000 mod 2^32)
+        const int32_t KB = (int32_t)(0u - 0x40000000u) + z0;
+        L.mL0 = (g == 0 && t != 0) ? KB - (1 << 27) : KB;
+        L.mL1 = g == 0 ? KB - (1 << 27) : KB;
+        L.mC0 = (g == 0 && t != 0) ? KB - (1 << 26) : KB;
+        L.mC1 = g == 0 ? KB - (1 << 26) : KB;
+        L.mK = KB;
     }
     {
         uint32_t r = 0;
@@ -674,11 +683,42 @@ __device__ void build_lane_const(LaneConst &L, const int8_t *__restrict__ T_all,
 #define VCA_F16P2 0
 #endif
 
+// Mixed 8-bit pass 2 (VCA_MIXP2, default): with the same pass-1 offsets as VCA_F16P2 (every Z' in
+// [0, 2^18)), the low byte of Z' goes through ONE s8 x u8 IMMA (the byte-plane path's plane 0)
+// and Z' >> 8 (< 1024) through ONE f16 HMMA as exact subnormals (f32 accumulator at 0.75, so the
+// result's bits are 0x3F400000 + S_hi, |S_hi| < 2^22); then C = E_lo + 256 bits(E_hi) with all
+// constants in the IMMA's accumulator init: 5 PRMT + 1 IMMA + 1 HMMA + 1 IMAD per 4 values instead
+// of 7 PRMT + 3 IMMA + 2 IMAD.  Exact (integer sums below 2^24 in f32), bit-identical results --
+// but one f32 HMMA costs the tensor pipe more than the two IMMAs it replaces: config 3 -4 %,
+// config 2 -6.6 % (profiles/r02/ab_mixed_pass2_reverted.log); off.
+#ifndef VCA_MIXP2
+#define VCA_MIXP2 0
+#endif
+
 template <int ES, bool PERM1 = false>
 __device__ __forceinline__ void dct16(const LaneConst &L, const uint32_t (&blo)[2], const uint32_t (&bhi)[2],
                                       int32_t (&C)[2][4])
 {
     int32_t D1[2][4];
+    if (ES == 1 && VCA_MIXP2 && !VCA_F16P2) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            mma16_su_c(D1[q], PERM1 ? L.p16a0 : L.t16a0, PERM1 ? L.p16a1 : L.t16a1, blo[q], L.zq[0], L.zq[1], L.zq[2],
+                       L.zq[3]);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const uint32_t v0 = D1[0][2 * p], v1 = D1[0][2 * p + 1], v2 = D1[1][2 * p], v3 = D1[1][2 * p + 1];
+            const uint32_t lo = __byte_perm(__byte_perm(v0, v1, 0x5140), __byte_perm(v2, v3, 0x5140), 0x5410);
+            const uint32_t h0 = __byte_perm(v0, v1, 0x6521), h1 = __byte_perm(v2, v3, 0x6521);
+            int32_t E0[4];
+            mma16_su_c(E0, L.p16a0, L.p16a1, lo, p == 0 ? L.mL0 : L.mL1, L.mL1, L.mK, L.mK);
+            float Eh[4];
+            mma16_hc(Eh, L.g16[0], L.g16[1], L.g16[2], L.g16[3], h0, h1, L.mq[0], L.mq[1], L.mq[2], L.mq[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) C[p][e] = (int32_t)((uint32_t)E0[e] + __float_as_uint(Eh[e]) * 256u);
+        }
+        return;
+    }
     if (ES == 1 && VCA_F16P2) {
 #pragma unroll
         for (int q = 0; q < 2; ++q)
@@ -733,6 +773,20 @@ template <int ES, bool PERM1 = false>
 __device__ __forceinline__ void dct8pair(const LaneConst &L, uint32_t blo, uint32_t bhi, int32_t (&C)[4])
 {
     int32_t D1[4];
+    if (ES == 1 && VCA_MIXP2 && !VCA_F16P2) {
+        // as dct16's mixed pass 2; V rows take the 2^17 offset also at k = 0 (the luma pass-1 quad)
+        mma16_su_c(D1, PERM1 ? L.p8a0 : L.t8a0, PERM1 ? L.p8a1 : L.t8a1, blo, L.zq[0], L.zq[1], L.zq[2], L.zq[3]);
+        const uint32_t lo =
+            __byte_perm(__byte_perm(D1[0], D1[1], 0x5140), __byte_perm(D1[2], D1[3], 0x5140), 0x5410);
+        const uint32_t h0 = __byte_perm(D1[0], D1[1], 0x6521), h1 = __byte_perm(D1[2], D1[3], 0x6521);
+        int32_t E0[4];
+        mma16_su_c(E0, L.p8a0, L.p8a1, lo, L.mC0, L.mC1, L.mC1, L.mC1);
+        float Eh[4];
+        mma16_hc(Eh, L.g8, 0u, 0u, L.g8, h0, h1, L.mq[0], L.mq[1], L.mq[2], L.mq[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) C[e] = (int32_t)((uint32_t)E0[e] + __float_as_uint(Eh[e]) * 256u);
+        return;
+    }
     if (ES == 1 && VCA_F16P2) {
         // V rows take the 2^17 offset also at k = 0 (Z_0 + 2^17 < 2^18 for n = 8), so the
         // pass-1 quad is the luma one; corrections: U C_0k (k != 0), V C_0k (all k)
