@@ -239,6 +239,126 @@ __global__ void k_ld_rate(int iters, long long *cycles, uint32_t *sink)
     if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
+// ---- 1b. TS mode: A (128 x 32 bytes) written into TMEM with tcgen05.st (thread m = lane m, word c =
+// K bytes 4c..4c+3, little endian), B from shared memory (K-major, no swizzle), D = A . B in TMEM
+__device__ __forceinline__ void mma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+template <int N>
+__global__ void k_correct_ts(const int8_t *A, const int8_t *Bt, int a_s8, int b_s8, int32_t *D, long long *cyc)
+{
+    __shared__ __align__(1024) uint8_t sB[N * 32];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int i = tid; i < N * 32; i += blockDim.x) {
+        const int n = i / 32, k = i % 32;
+        sB[kmaj(n, k, 128, 256)] = (uint8_t)Bt[i];
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(&tbase, 256);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tm = tbase;
+    // A row m = 32 warp + lane into TMEM columns [128, 136)
+    {
+        uint32_t w[8];
+        const uint8_t *row = reinterpret_cast<const uint8_t *>(A) + (32 * warp + lane) * 32;
+        for (int c = 0; c < 8; ++c)
+            w[c] = (uint32_t)row[4 * c] | ((uint32_t)row[4 * c + 1] << 8) | ((uint32_t)row[4 * c + 2] << 16) |
+                   ((uint32_t)row[4 * c + 3] << 24);
+        const uint32_t ta = tm + ((uint32_t)(32 * warp) << 16) + 128;
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(w[0]),
+                     "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                     : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (tid == 0) {
+        const uint64_t bd = sdesc(smem_u32(sB), 128, 256);
+        const uint32_t id = idesc_i8(128, N, a_s8, b_s8, false, false);
+        mma_i8_ts(tm, tm + 128, bd, id, 0);
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        // rate: 256 dependent-free TS MMAs into 4 accumulators
+        const long long t0 = clock64();
+        for (int i = 0; i < 256; ++i) mma_i8_ts(tm + 160 + (i & 1) * 32, tm + 128, bd, id, 1);
+        mma_commit(&bar);
+        mbar_wait(&bar, 1);
+        cyc[0] = clock64() - t0;
+    }
+    fence_before();
+    __syncthreads();  // thread 0 has seen both MMA phases complete
+    fence_after();
+    for (int c = 0; c < N; c += 32) {
+        uint32_t r[32];
+        LD32(tm + ((uint32_t)(32 * warp) << 16) + c, r);
+        tmem_wait_ld();
+        for (int j = 0; j < 32 && c + j < N; ++j) D[(32 * warp + lane) * N + c + j] = (int32_t)r[j];
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tm, 256);
+}
+
+template <int N>
+bool run_correct_ts(int a_s8, int b_s8)
+{
+    std::vector<int8_t> A(128 * 32), Bt(N * 32);
+    srand(777 + N);
+    for (auto &v : A) v = (int8_t)(rand() & 255);
+    for (auto &v : Bt) v = (int8_t)(rand() & 255);
+    int8_t *dA, *dB;
+    int32_t *dD;
+    long long *dc;
+    CK(cudaMalloc(&dA, A.size()));
+    CK(cudaMalloc(&dB, Bt.size()));
+    CK(cudaMalloc(&dD, 128 * N * 4));
+    CK(cudaMalloc(&dc, 8));
+    CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, Bt.data(), Bt.size(), cudaMemcpyHostToDevice));
+    k_correct_ts<N><<<1, 128>>>(dA, dB, a_s8, b_s8, dD, dc);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    std::vector<int32_t> D(128 * N);
+    long long cyc = 0;
+    CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+    int bad = 0;
+    for (int m = 0; m < 128; ++m)
+        for (int n = 0; n < N; ++n) {
+            int64_t s = 0;
+            for (int k = 0; k < 32; ++k) {
+                const int a = a_s8 ? (int)A[m * 32 + k] : (int)(uint8_t)A[m * 32 + k];
+                const int b = b_s8 ? (int)Bt[n * 32 + k] : (int)(uint8_t)Bt[n * 32 + k];
+                s += a * b;
+            }
+            if ((int32_t)s != D[m * N + n]) {
+                if (bad < 4) printf("  mismatch m=%d n=%d got %d want %lld\n", m, n, D[m * N + n], (long long)s);
+                ++bad;
+            }
+        }
+    printf("correct TS (A in TMEM via tcgen05.st) N=%d A %s, B %s: %s (%d bad); %.1f cycles per TS MMA (1 CTA)\n", N,
+           a_s8 ? "s8" : "u8", b_s8 ? "s8" : "u8", bad ? "FAIL" : "ok", bad, cyc / 256.0);
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dD);
+    cudaFree(dc);
+    return bad == 0;
+}
+
 template <int N>
 bool run_correct(int a_mn, int a_s8, int b_s8)
 {
@@ -323,6 +443,7 @@ void run_ld_rate(int warps, int sms)
 
 int main()
 {
+    setvbuf(stdout, NULL, _IONBF, 0);
     int dev = 0, sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     bool ok = true;
@@ -332,6 +453,8 @@ int main()
     ok &= run_correct<64>(0, 1, 0);
     ok &= run_correct<16>(0, 0, 1);
     ok &= run_correct<32>(1, 1, 1);
+    ok &= run_correct_ts<32>(1, 0);
+    ok &= run_correct_ts<32>(0, 1);
     printf("descriptor correctness: %s\n", ok ? "all ok" : "FAILURES");
     run_mma_rate<32, 2>(sms);
     run_mma_rate<32, 8>(sms);
