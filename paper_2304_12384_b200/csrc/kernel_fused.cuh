@@ -94,6 +94,21 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// One 4-D tensor-map load of a strip's NB boxes of a plane (dims: bytes within a box row, rows,
+// box index along the row, frame): the same smem layout as NB 3-D box loads, one TMA instruction
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c, int y, int z,
+                                            uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(c), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+#ifndef VCA_TMA4
+#define VCA_TMA4 1  // use the 4-D maps where the plane geometry allows (A/B: 0 = always 3-D)
+#endif
+
 // L2 prefetch of a box a few strips ahead of the ring (VCA_L2PF strips; 0 = off): the later
 // TMA load of the same box then hits L2 instead of HBM.  A/B (profiles/r02/ab_l2_prefetch_reverted.log,
 // 1 / 2 / 4 strips ahead): config 3 -4 %, config 4 -2..-4 %, config 2 -2 % -- off.
@@ -912,6 +927,7 @@ struct FusedArgs {
     // this launch owns tickets [ticket_base, ticket_base + items + groups)
     unsigned long long *ticket;
     unsigned long long ticket_base;
+    int y4, c4;  // the Y / chroma tensor maps are 4-D (one load per plane per strip)
 };
 
 // Work distribution over the consumer groups.  0: static round robin (item it goes to virtual
@@ -1571,16 +1587,25 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     if (s > 0 && !first_pass) mbar_wait(smem_u32(&empty[st]), phase ^ 1);
                     uint8_t *base = smem + st * F::STAGE;
                     mbar_expect_tx(&full[st], F::TX);
+                    if (a.y4) {
+                        tma_load_4d(base, &tmY, &full[st], s * F::NBOX_Y, r * W, f, policy);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < F::NBOX_Y; ++b)
-                        tma_load_3d(base + b * F::BOXB_Y, &tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * W,
-                                    r * W, f, policy);
+                        for (int b = 0; b < F::NBOX_Y; ++b)
+                            tma_load_3d(base + b * F::BOXB_Y, &tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * W,
+                                        r * W, f, policy);
+                    }
+                    if (a.c4) {
+                        tma_load_4d(base + F::ST_Y, &tmU, &full[st], s * F::NBOX_C, r * WC, f, policy);
+                        tma_load_4d(base + F::ST_Y + F::ST_C, &tmV, &full[st], s * F::NBOX_C, r * WC, f, policy);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < F::NBOX_C; ++b) {
-                        tma_load_3d(base + F::ST_Y + b * F::BOXB_C, &tmU, &full[st],
-                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
-                        tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
-                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                        for (int b = 0; b < F::NBOX_C; ++b) {
+                            tma_load_3d(base + F::ST_Y + b * F::BOXB_C, &tmU, &full[st],
+                                        (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                            tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
+                                        (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                        }
                     }
                     if (++st == F::STAGES) {
                         st = 0;
@@ -1634,16 +1659,25 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     continue;
 #endif
                     mbar_expect_tx(&full[st], F::TX);
+                    if (a.y4) {
+                        tma_load_4d(base, &tmY, &full[st], s * F::NBOX_Y, r * W, f, policy);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < F::NBOX_Y; ++b)
-                        tma_load_3d(base + b * F::BOXB_Y, &tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * W,
-                                    r * W, f, policy);
+                        for (int b = 0; b < F::NBOX_Y; ++b)
+                            tma_load_3d(base + b * F::BOXB_Y, &tmY, &full[st], (s * F::UNITS + b * F::UPB_Y) * W,
+                                        r * W, f, policy);
+                    }
+                    if (a.c4) {
+                        tma_load_4d(base + F::ST_Y, &tmU, &full[st], s * F::NBOX_C, r * WC, f, policy);
+                        tma_load_4d(base + F::ST_Y + F::ST_C, &tmV, &full[st], s * F::NBOX_C, r * WC, f, policy);
+                    } else {
 #pragma unroll
-                    for (int b = 0; b < F::NBOX_C; ++b) {
-                        tma_load_3d(base + F::ST_Y + b * F::BOXB_C, &tmU, &full[st],
-                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
-                        tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
-                                    (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                        for (int b = 0; b < F::NBOX_C; ++b) {
+                            tma_load_3d(base + F::ST_Y + b * F::BOXB_C, &tmU, &full[st],
+                                        (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                            tma_load_3d(base + F::ST_Y + F::ST_C + b * F::BOXB_C, &tmV, &full[st],
+                                        (s * F::UNITS + b * F::UPB_C) * WC, r * WC, f, policy);
+                        }
                     }
                     if (++st == F::STAGES) {
                         st = 0;
@@ -2034,10 +2068,16 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
 {
     using F = Fam<W, BD, LP>;
     CUtensorMap mY, mU, mV;
-    if (!make_map(&mY, pl.p[0], n_frames, F::ES, F::IB_Y, W) || !make_map(&mU, pl.p[1], n_frames, F::ES, F::IB_C, W / 2) ||
-        !make_map(&mV, pl.p[2], n_frames, F::ES, F::IB_C, W / 2))
+    int y4 = 0, u4 = 0, v4 = 0;
+    if (!make_plane_map(&mY, pl.p[0], n_frames, F::ES, F::IB_Y, W, F::NBOX_Y, &y4) ||
+        !make_plane_map(&mU, pl.p[1], n_frames, F::ES, F::IB_C, W / 2, F::NBOX_C, &u4) ||
+        !make_plane_map(&mV, pl.p[2], n_frames, F::ES, F::IB_C, W / 2, F::NBOX_C, &v4))
         return -2;
+    if (u4 != v4 && !make_map(u4 ? &mU : &mV, u4 ? pl.p[1] : pl.p[2], n_frames, F::ES, F::IB_C, W / 2))
+        return -2;  // (U and V share one flag; equal geometry makes this unreachable)
     FusedArgs a;
+    a.y4 = y4;
+    a.c4 = u4 && v4;
     a.n_frames = n_frames;
     for (int p = 0; p < 3; ++p) {
         a.width[p] = pl.p[p].width;
@@ -2071,6 +2111,46 @@ inline int launch_one(const Planes3 &pl, int n_frames, const int8_t *T, const do
     // every group takes exactly one ticket past the last item: the next launch starts after them
     if (ticket_base) *ticket_base += (unsigned long long)items + (unsigned long long)grid * F::GV;
     return 0;
+}
+
+// 4-D map of a plane (bytes within a box row, rows, box index along the row, frame): one TMA loads a
+// strip's nb boxes into the same smem layout as nb 3-D loads.  Used when every box is whole (row
+// bytes a multiple of the box width: no box reads past a row) and boxes have >= 8 rows (the smem
+// box stride of the 4-row chroma boxes of the w = 8 family is padded to 8 rows).
+inline bool map4_ok(const PlaneDesc &P, int es, int inner_bytes, int box_rows, int nb)
+{
+    return VCA_TMA4 && nb > 1 && box_rows >= 8 && ((int64_t)P.width * es) % inner_bytes == 0;
+}
+
+inline bool make_map4(CUtensorMap *m, const PlaneDesc &P, int n_frames, int es, int inner_bytes, int box_rows, int nb)
+{
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)(inner_bytes / es), (cuuint64_t)P.height,
+                          (cuuint64_t)(((int64_t)P.width * es) / inner_bytes), (cuuint64_t)n_frames};
+    cuuint64_t strides[3] = {(cuuint64_t)P.pitch, (cuuint64_t)inner_bytes,
+                             (cuuint64_t)(P.fstride > 0 ? P.fstride : P.pitch * P.height)};
+    cuuint32_t box[4] = {(cuuint32_t)(inner_bytes / es), (cuuint32_t)box_rows, (cuuint32_t)nb, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUtensorMapSwizzle sw = inner_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : inner_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+    CUresult r = enc(m, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
+                     const_cast<uint8_t *>(P.base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// the plane's map: 4-D when map4_ok and encodable, else 3-D; *four says which
+inline bool make_plane_map(CUtensorMap *m, const PlaneDesc &P, int n_frames, int es, int inner_bytes, int box_rows,
+                           int nb, int *four)
+{
+    if (map4_ok(P, es, inner_bytes, box_rows, nb) && make_map4(m, P, n_frames, es, inner_bytes, box_rows, nb)) {
+        *four = 1;
+        return true;
+    }
+    *four = 0;
+    return make_map(m, P, n_frames, es, inner_bytes, box_rows);
 }
 
 template <int W, int BD, int LP>
