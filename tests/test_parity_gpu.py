@@ -85,8 +85,8 @@ CASES_STRIPS = [
     # row bytes a multiple of the box width: the 4-D tensor-map loads (one TMA per plane per
     # strip); partial last block row, ragged last strip
     ("tma4_lp16", 1152, 70, 8, 16, True),              # 72 cols: 4 x 16 + 8; Y 4-D, chroma 3-D
-    ("tma4_full16_8bit", 1152, 40, 8, 16, False),      # Y and chroma 4-D
-    ("tma4_full16_10bit", 640, 40, 10, 16, False),     # 40 cols: 2 x 16 + 8
+    ("tma4_full16_8bit", 1152, 40, 8, 16, False),      # Y 4-D, chroma 3-D (one box per strip)
+    ("tma4_full16_10bit", 640, 40, 10, 16, False),     # 40 cols: 2 x 16 + 8; Y and chroma 4-D
     ("tma4_lp32_10bit", 1024, 68, 10, 32, True),
     ("tma4_full32", 1280, 76, 8, 32, False),           # 40 cols: 5 x 8; Y 4-D, chroma 3-D (640 B rows)
 ]
