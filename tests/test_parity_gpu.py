@@ -420,3 +420,24 @@ def test_concurrent_contexts_on_streams():
         outs.append((records_to_numpy(r1), records_to_numpy(r2)))
     for r1, r2 in outs:
         assert r1.tobytes() == seq[0].tobytes() and r2.tobytes() == seq[1].tobytes()
+
+
+@pytest.mark.parametrize("W,H,bd,w,lp", [(1024, 72, 8, 32, True), (640, 40, 10, 16, False), (1152, 70, 8, 16, True)])
+def test_parity_padded_pitch_tma4(W, H, bd, w, lp):
+    """4-D tensor-map geometry (row bytes a multiple of the box width) with a row pitch well above
+    the row bytes and a frame stride above H x pitch: records against the oracle, production vs
+    DUMP bit for bit, every block's integer checks."""
+    F = 3
+    Y, U, V = synth.g_frames(37, W, H, F, bd)
+    padded = []
+    for p in (Y, U, V):
+        f, h, wd = p.shape
+        buf = torch.zeros((f, h + 3, wd + 256 // p.element_size()), dtype=p.dtype, device="cuda")
+        buf[:, :h, :wd] = p.cuda()
+        padded.append(buf[:, :h, :wd])
+    pair = Pair(W, H, bd, w, lp)
+    rec, hy, ch = pair.analyze(*padded)
+    ro, rhy, rch = oracle_checks(Y, U, V, bd, w, lp)
+    assert_records(rec, ro)
+    assert_records(rec, ro, rtol=1e-12)
+    assert_checks(ch, rch)
