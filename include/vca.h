@@ -24,7 +24,9 @@
  *  - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
  *    stream) and the call returns after launch; results are valid once the
  *    stream is synchronised.  A context must not be used from two threads
- *    at once.
+ *    at once, and its calls must execute in call order on the device (one
+ *    stream, or streams ordered by events): each call reads the previous
+ *    frame's energies the call before it left in the context (R-7).
  *  - Results are bit-identical for any split of a sequence into calls, any
  *    frame-range partition across GPUs (with a one-frame halo) and any
  *    launch configuration.
