@@ -346,3 +346,30 @@ def test_y4m_parameterised_markers_with_fixed_size(tmp_path):
                 break
         Y = np.concatenate([g[0] for g in got])
     assert np.array_equal(Y[:4], planes[0])
+
+
+def test_y4m_first_failure_is_deterministic(tmp_path):
+    """A valid Y4M whose frame 20 carries a parameterised marker, in a file whose size divides
+    into bare-marker records: the positional readers (16 threads) see frame 20 as the end of the
+    fixed-size run and every later record as misaligned; the first failing frame and its own
+    status must win together (one packed atomic), so every read falls back to the sequential
+    reader at frame 20 and delivers all 64 frames -- never the misaligned records' status."""
+    F = 64
+    planes = frames_420(F, 16, 8, 8, seed=9)
+    fb = 16 * 8 * 3 // 2
+    head = b"YUV4MPEG2 W16 H8 F25:1 C420jpeg\n"
+    recs = [(b"FRAME Ip\n" if t == 20 else b"FRAME\n") + b"".join(p[t].tobytes() for p in planes) for t in range(F)]
+    data = head + b"".join(recs)
+    pad = (6 + fb) - (len(data) - len(head)) % (6 + fb)
+    data += b"FRAME\n" + bytes(pad - 6)
+    f = tmp_path / "race.y4m"
+    f.write_bytes(data)
+    for _ in range(20):
+        with vcaio.Reader(str(f), "y4m") as r:
+            got = []
+            while r.frames < F:
+                rc, fr = r.read(F - r.frames)
+                assert rc == vcaio.VCA_OK, (rc, r.frames)
+                got.append(fr[0])
+            Y = np.concatenate(got)
+        assert np.array_equal(Y[:F], planes[0])
