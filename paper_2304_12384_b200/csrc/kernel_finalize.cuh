@@ -23,7 +23,12 @@ struct FinalizeArgs {
     double *saveHY;        // receives the last frame's H_Y (the next call's prevHY; another buffer)
     int64_t first_poc;
     vca_features *out;
+    int frames_per_cta;    // consecutive frames per CTA (> 1 only when C_Y <= kFinalizeThreads * kHYRegs)
 };
+
+// A CTA that finalizes several consecutive frames keeps the previous frame's H_Y in registers
+// (kHYRegs per thread), so each frame's H_Y is read from memory once instead of twice.
+constexpr int kHYRegs = 32;
 
 template <int K>
 __device__ __forceinline__ void block_reduce(double (&v)[K], double (*sm)[kFinalizeThreads / 32])
@@ -45,37 +50,12 @@ __device__ __forceinline__ void block_reduce(double (&v)[K], double (*sm)[kFinal
     }
 }
 
-__global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs a)
+// One frame's record from its partial sums and h SAD (v[0..6]), fixed-order block reduction.
+__device__ __forceinline__ void emit_record(const FinalizeArgs &a, int f, bool have_prev, double (&v)[7],
+                                            double (*sm)[kFinalizeThreads / 32])
 {
-    __shared__ double sm[7][kFinalizeThreads / 32];
-    const int f = blockIdx.x;
-    const int tid = threadIdx.x;
-    double v[7];
-#pragma unroll
-    for (int q = 0; q < 7; ++q) v[q] = 0.0;
-    // partial sums of the block kernel, plane by plane, in index order per thread
-#pragma unroll
-    for (int p = 0; p < 3; ++p) {
-        const double *pp = a.s.partial + ((int64_t)f * 3 + p) * a.s.P * 2;
-        for (int q = tid; q < a.s.Pp[p]; q += kFinalizeThreads) {
-            v[2 * p] += pp[2 * q];
-            v[2 * p + 1] += pp[2 * q + 1];
-        }
-    }
-    // h: SAD against the previous frame's luma energies (R-7)
-    const double *cur = a.s.HY + (int64_t)f * a.count[0];
-    const double *prev = f > 0 ? cur - a.count[0] : a.prevHY;
-    if (prev) {
-        for (int64_t k = tid; k < a.count[0]; k += kFinalizeThreads) v[6] += fabs(cur[k] - prev[k]);
-    }
-    {  // carry the last frame's H_Y to the next call (R-7): every CTA copies a slice
-        const double *last = a.s.HY + (int64_t)(a.n_frames - 1) * a.count[0];
-        const int64_t per = (a.count[0] + a.n_frames - 1) / a.n_frames;
-        const int64_t k0 = (int64_t)f * per, k1 = min(a.count[0], k0 + per);
-        for (int64_t k = k0 + tid; k < k1; k += kFinalizeThreads) a.saveHY[k] = last[k];
-    }
     block_reduce<7>(v, sm);
-    if (tid == 0 && f >= a.n_halo) {
+    if (threadIdx.x == 0 && f >= a.n_halo) {
         vca_features r;
         r.poc = a.first_poc + (f - a.n_halo);
         const double nY = (double)a.n[0], nU = (double)a.n[1], nV = (double)a.n[2];
@@ -85,8 +65,77 @@ __global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs
         r.L_U = v[3] / (double)a.count[1];
         r.E_V = v[4] / ((double)a.count[2] * nV * nV);
         r.L_V = v[5] / (double)a.count[2];
-        r.h = prev ? v[6] / ((double)a.count[0] * nY * nY) : 0.0;
+        r.h = have_prev ? v[6] / ((double)a.count[0] * nY * nY) : 0.0;
         a.out[f - a.n_halo] = r;
+    }
+    __syncthreads();  // sm is reused by the next frame
+}
+
+__device__ __forceinline__ void partial_sums(const FinalizeArgs &a, int f, double (&v)[7])
+{
+#pragma unroll
+    for (int q = 0; q < 7; ++q) v[q] = 0.0;
+    // partial sums of the block kernel, plane by plane, in index order per thread
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+        const double *pp = a.s.partial + ((int64_t)f * 3 + p) * a.s.P * 2;
+        for (int q = threadIdx.x; q < a.s.Pp[p]; q += kFinalizeThreads) {
+            v[2 * p] += pp[2 * q];
+            v[2 * p + 1] += pp[2 * q + 1];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kFinalizeThreads) finalize_kernel(FinalizeArgs a)
+{
+    __shared__ double sm[7][kFinalizeThreads / 32];
+    const int tid = threadIdx.x;
+    double v[7];
+    {  // carry the last frame's H_Y to the next call (R-7): every CTA copies a slice
+        const double *last = a.s.HY + (int64_t)(a.n_frames - 1) * a.count[0];
+        const int64_t per = (a.count[0] + gridDim.x - 1) / gridDim.x;
+        const int64_t k0 = (int64_t)blockIdx.x * per, k1 = min(a.count[0], k0 + per);
+        for (int64_t k = k0 + tid; k < k1; k += kFinalizeThreads) a.saveHY[k] = last[k];
+    }
+    if (a.frames_per_cta <= 1) {
+        const int f = blockIdx.x;
+        partial_sums(a, f, v);
+        // h: SAD against the previous frame's luma energies (R-7)
+        const double *cur = a.s.HY + (int64_t)f * a.count[0];
+        const double *prev = f > 0 ? cur - a.count[0] : a.prevHY;
+        if (prev) {
+            for (int64_t k = tid; k < a.count[0]; k += kFinalizeThreads) v[6] += fabs(cur[k] - prev[k]);
+        }
+        emit_record(a, f, prev != nullptr, v, sm);
+        return;
+    }
+    // frames f0 .. f0 + frames_per_cta - 1: the previous frame's H_Y stays in registers (the same
+    // per-thread index order k = tid + 256 i as above, so the sums are bit-identical)
+    const int f0 = blockIdx.x * a.frames_per_cta;
+    const int f1 = min(a.n_frames, f0 + a.frames_per_cta);
+    const int C = (int)a.count[0];
+    double hp[kHYRegs];
+    const double *prev0 = f0 > 0 ? a.s.HY + (int64_t)(f0 - 1) * C : a.prevHY;
+    bool have_prev = prev0 != nullptr;
+#pragma unroll
+    for (int i = 0; i < kHYRegs; ++i) {
+        const int k = tid + i * kFinalizeThreads;
+        hp[i] = (have_prev && k < C) ? prev0[k] : 0.0;
+    }
+    for (int f = f0; f < f1; ++f) {
+        partial_sums(a, f, v);
+        const double *cur = a.s.HY + (int64_t)f * C;
+#pragma unroll
+        for (int i = 0; i < kHYRegs; ++i) {
+            const int k = tid + i * kFinalizeThreads;
+            if (k < C) {
+                const double x = cur[k];
+                if (have_prev) v[6] += fabs(x - hp[i]);
+                hp[i] = x;
+            }
+        }
+        emit_record(a, f, have_prev, v, sm);
+        have_prev = true;
     }
 }
 

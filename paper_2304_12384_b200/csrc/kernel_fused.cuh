@@ -105,6 +105,23 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(c), "r"(z), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// Stores of the per-block H_Y and the per-row partials that the finalize kernel reads right
+// after this kernel: with VCA_EVICT_LAST they carry an L2 evict_last hint (the frames stream
+// through L2 evict_first), so the finalize reads them from L2.  A/B: block kernel -1.4 %,
+// finalize unchanged (profiles/r02/ab_evict_last_reverted.log); off.
+#ifndef VCA_EVICT_LAST
+#define VCA_EVICT_LAST 0
+#endif
+__device__ __forceinline__ void st_keep(double *p, double v, uint64_t pol)
+{
+#if VCA_EVICT_LAST
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+    (void)pol;
+    *p = v;
+#endif
+}
+
 #ifndef VCA_TMA4
 #define VCA_TMA4 1  // use the 4-D maps where the plane geometry allows (A/B: 0 = always 3-D)
 #endif
@@ -1735,6 +1752,10 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
     const uint32_t smem0 = smem_off(smem);  // stage boxes: data offsets
     const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
     const int64_t CY = (int64_t)rows * cols;
+    uint64_t keep = 0;
+#if VCA_EVICT_LAST
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+#endif
 
     // per-warp constants: smem offsets of this warp's units inside a stage, and the number of
     // leading strips in which all NU units of this warp are whole (valid, not a partial
@@ -1952,7 +1973,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
 #ifdef VCA_DEBUG_BOUNDS
                     if (cl < 0 || cl >= cols) __trap();
 #endif
-                    HYrow[cl] = Hl;
+                    st_keep(HYrow + cl, Hl, keep);
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -1990,12 +2011,12 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
             double *P0 = a.s.partial + (((int64_t)f * 3 + 0) * a.s.P + q) * 2;
             double *P1 = a.s.partial + (((int64_t)f * 3 + 1) * a.s.P + q) * 2;
             double *P2 = a.s.partial + (((int64_t)f * 3 + 2) * a.s.P + q) * 2;
-            P0[0] = sHY;
-            P0[1] = sLY;
-            P1[0] = hu;
-            P1[1] = sLU;
-            P2[0] = hv;
-            P2[1] = sLV;
+            st_keep(P0, sHY, keep);
+            st_keep(P0 + 1, sLY, keep);
+            st_keep(P1, hu, keep);
+            st_keep(P1 + 1, sLU, keep);
+            st_keep(P2, hv, keep);
+            st_keep(P2 + 1, sLV, keep);
         }
     }
 }

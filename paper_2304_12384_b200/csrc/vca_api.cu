@@ -64,6 +64,10 @@ struct vca_ctx {
 
 namespace {
 
+#ifndef VCA_FIN_FRAMES
+#define VCA_FIN_FRAMES 1  // max consecutive frames per finalize CTA (power of two; A/B: 2, 4 slower -- latency-bound chain)
+#endif
+
 int fail_cuda(vca_ctx *ctx, cudaError_t e)
 {
     if (e != cudaSuccess) {
@@ -272,7 +276,16 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
     fa.saveHY = ctx->d_prevHY + (1 - ctx->cur_prev) * CY;
     fa.first_poc = ctx->next_poc;
     fa.out = out;
-    finalize_kernel<<<n_frames, kFinalizeThreads, 0, st>>>(fa);
+    // several consecutive frames per CTA (each H_Y read once) while the grid still covers the SMs
+    fa.frames_per_cta = 1;
+    if (CY <= (size_t)kFinalizeThreads * kHYRegs)
+        for (int k = VCA_FIN_FRAMES; k > 1; k >>= 1)
+            if (n_frames >= k * ctx->sm_count) {
+                fa.frames_per_cta = k;
+                break;
+            }
+    const int fin_grid = (n_frames + fa.frames_per_cta - 1) / fa.frames_per_cta;
+    finalize_kernel<<<fin_grid, kFinalizeThreads, 0, st>>>(fa);
     VCA_CK(ctx, cudaGetLastError());
     ctx->launches += 1;
     if (prof) {
