@@ -2045,6 +2045,10 @@ inline PFN_encodeTiled get_encode()
     return fn;
 }
 
+#ifndef VCA_L2PROMO
+#define VCA_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B  // A/B: NONE / L2_64B / L2_128B / L2_256B
+#endif
+
 inline bool make_map(CUtensorMap *m, const PlaneDesc &P, int n_frames, int es, int inner_bytes, int box_rows)
 {
     PFN_encodeTiled enc = get_encode();
@@ -2058,7 +2062,7 @@ inline bool make_map(CUtensorMap *m, const PlaneDesc &P, int n_frames, int es, i
                                                 : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = enc(m, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
                      const_cast<uint8_t *>(P.base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     VCA_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -2158,7 +2162,7 @@ inline bool make_map4(CUtensorMap *m, const PlaneDesc &P, int n_frames, int es, 
                                                 : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = enc(m, es == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 4,
                      const_cast<uint8_t *>(P.base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     VCA_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
