@@ -327,7 +327,15 @@ struct Fam {
 #endif
     static constexpr int MINB = VCA_MINB;  // CTAs/SM of the legacy layout (kGroups == 0)
     // per consumer warp: [32 slots][9] doubles (8 luma row-group partials + pad) + [32][4] DC words
-    static constexpr int STASH = 32 * 9 * 8 + 32 * 4 * 4;
+    // luma H partials stashed per unit: one per row group (the 4 lanes of a row group reduced by
+    // shuffles) or, with VCA_HHALF on the n = 16 luma families, one per half row group (lanes t = 0,
+    // 2 after one shuffle round; the flush adds 16 instead of 8)
+#ifndef VCA_HHALF
+#define VCA_HHALF 1
+#endif
+    static constexpr int HSLOTS = (VCA_HHALF && NY == 16 && LP) ? 16 : 8;  // (w = 16 full: over the smem limit)
+    static constexpr int HW = HSLOTS + 1;  // padded row of the stash
+    static constexpr int STASH = 32 * HW * 8 + 32 * 4 * 4;
     static_assert(NC == NY / 2, "chroma DCT is half the luma DCT");
     static_assert(IB_Y == 32 || IB_Y == 64 || IB_Y == 128, "swizzle span");
     static_assert(IB_C == 32 || IB_C == 64 || IB_C == 128, "swizzle span");
@@ -1190,9 +1198,10 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
     }
 #pragma unroll
     for (int n = 0; n < NU; ++n) {
-        // reduce over the 4 lanes of a row group: lanes t == 0 hold the partial of rows g (+8, ...)
+        // reduce over the 4 lanes of a row group (lanes t == 0 hold the partial of rows g (+8, ...)),
+        // or over lane pairs (HSLOTS == 16: lanes t = 0, 2 hold half a row group each)
         hY[n] += __shfl_xor_sync(0xffffffffu, hY[n], 1);
-        hY[n] += __shfl_xor_sync(0xffffffffu, hY[n], 2);
+        if (F::HSLOTS == 8) hY[n] += __shfl_xor_sync(0xffffffffu, hY[n], 2);
         o[n].hY = hY[n];
     }
 
@@ -1333,7 +1342,7 @@ __device__ __forceinline__ void process_units(const UnitCtx<F> &U, const FusedAr
         for (int n = 0; n < NU; ++n) {
             double hy = hY[n], hu = o[n].hu, hv = o[n].hv;
 #pragma unroll
-            for (int s = 4; s < 32; s <<= 1) hy += __shfl_xor_sync(0xffffffffu, hy, s);
+            for (int s = F::HSLOTS == 8 ? 4 : 2; s < 32; s <<= 1) hy += __shfl_xor_sync(0xffffffffu, hy, s);
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) {
                 hu += __shfl_xor_sync(0xffffffffu, hu, s);
@@ -1712,8 +1721,11 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
     if constexpr (kGroups != 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Regs<F>::C));
     const int u = kGroups ? (warp & 3) : warp - 1;
     const int g = lane >> 2, t = lane & 3;
-    const uint32_t hst = smem_off(stash) + (grp * 4 + u) * F::STASH;  // [32][9] doubles
-    const uint32_t sxs = hst + 32 * 9 * 8;                 // [32][4] uint32
+    const uint32_t hst = smem_off(stash) + (grp * 4 + u) * F::STASH;  // [32][HW] doubles
+    const uint32_t sxs = hst + 32 * F::HW * 8;             // [32][4] uint32
+    // this lane's H partial slot within a unit's stash row (-1: the lane does not store)
+    const bool hst_lane = F::HSLOTS == 8 ? t == 0 : (t & 1) == 0;
+    const int hst_col = F::HSLOTS == 8 ? g : 2 * g + (t >> 1);
     UnitCtx<F> U;
     build_lane_const(U.L, a.T_all, g, t, NY);
     // per-lane scaled weights (A5): luma n = 16 positions (i = g + 8(e>>1), j = 8p + 2t + (e&1)),
@@ -1865,7 +1877,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     const uint32_t slm = sl0 + 4 * m;
 #pragma unroll
                     for (int n = 0; n < 4; ++n) {
-                        if (t == 0) sts<double>(hst + ((slm + n) * 9 + g) * 8, hY4[n]);
+                        if (t == 0) sts<double>(hst + ((slm + n) * F::HW + g) * 8, hY4[n]);
                         if (lane == 0) sts<uint32_t>(sxs + (slm + n) * 16, (uint32_t)dY[n]);
                     }
                     if ((g & 3) == 0 && (t & 1) == 0) {  // chroma DCs: units t >> 1 and 2 + (t >> 1), plane g >> 2
@@ -1888,7 +1900,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                 const uint32_t sl0 = (uint32_t)((s % F::SPF) * NU);
 #pragma unroll
                 for (int n = 0; n < NU; ++n) {
-                    if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, o[n].hY);
+                    if (hst_lane) sts<double>(hst + ((sl0 + n) * F::HW + hst_col) * 8, o[n].hY);
                     if (lane == 0) sts<uint4>(sxs + (sl0 + n) * 16, make_uint4(o[n].dcY, o[n].dcU, o[n].dcV, 0u));
                 }
             } else {
@@ -1912,7 +1924,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     const uint32_t sl0 = (uint32_t)((s % F::SPF) * NU);
 #pragma unroll
                     for (int n = 0; n < 2; ++n) {
-                        if (t == 0) sts<double>(hst + ((sl0 + n) * 9 + g) * 8, o2[n].hY);
+                        if (hst_lane) sts<double>(hst + ((sl0 + n) * F::HW + hst_col) * 8, o2[n].hY);
                         if (lane == 0)
                             sts<uint4>(sxs + (sl0 + n) * 16, make_uint4(o2[n].dcY, o2[n].dcU, o2[n].dcV, 0u));
                     }
@@ -1934,7 +1946,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                     else
                         process_units<F, false, DUMP, 1>(U, a, bY, bU, uY, uC, hvY, hvC, W, WC, kk, o1, hu, hv, ca);
                     const uint32_t slot = (uint32_t)((s % F::SPF) * NU + n);
-                    if (t == 0) sts<double>(hst + (slot * 9 + g) * 8, o1[0].hY);
+                    if (hst_lane) sts<double>(hst + (slot * F::HW + hst_col) * 8, o1[0].hY);
                     if (lane == 0) sts<uint4>(sxs + slot * 16, make_uint4(o1[0].dcY, o1[0].dcU, o1[0].dcV, 0u));
                 }
             }
@@ -1964,7 +1976,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
                 double Hl = 0.0, LYl = 0.0, LUl = 0.0, LVl = 0.0;
                 if (lane < nwin && cl < cols) {
 #pragma unroll
-                    for (int gg = 0; gg < 8; ++gg) Hl += lds_f64(hst + (lane * 9 + gg) * 8);
+                    for (int gg = 0; gg < F::HSLOTS; ++gg) Hl += lds_f64(hst + (lane * F::HW + gg) * 8);
                     // A6: sum x = C_00 / 4096 exactly (C_00 mod 2^32 suffices: sum x < 2^20, R-11)
                     const uint4 dc = lds<uint4>(sxs + lane * 16);
                     LYl = sqrt((double)(dc.x >> 12) * invNY);
