@@ -939,6 +939,34 @@ __device__ __forceinline__ void dct4oct(const LaneConst &L, uint32_t blo, uint32
     for (int e = 0; e < 4; ++e) C[e] = combine3(E0[e], E1[e], E2[e]);
 }
 
+// Cross-lane sums of a warp's 6 per-item partials in one reduce-scatter (VCA_XRED8): 8 values
+// (6 used) over 32 lanes; each xor round halves the values a lane carries (lanes keep one half
+// and receive the partner's copy of it), so 4 + 2 + 1 + 1 + 1 = 9 double shuffles instead of
+// 6 x 5.  Lane l ends with the total of value (l >> 2) & 7; the order is fixed.
+#ifndef VCA_XRED8
+#define VCA_XRED8 1
+#endif
+__device__ __forceinline__ double xred8(const double (&v)[8], int lane)
+{
+    const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+    double k[4], m[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? v[i] : v[i + 4], keep = b4 ? v[i + 4] : v[i];
+        k[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? k[i] : k[i + 2], keep = b3 ? k[i + 2] : k[i];
+        m[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const double send = b2 ? m[0] : m[1], keep = b2 ? m[1] : m[0];
+    double n = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    n += __shfl_xor_sync(0xffffffffu, n, 2);
+    n += __shfl_xor_sync(0xffffffffu, n, 1);
+    return n;
+}
+
 // ------------------------------------------------------------------ kernel
 struct FusedArgs {
     int n_frames;
@@ -1819,7 +1847,9 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
         ChromaAcc<F> ca;                                    // exact per-position chroma |C| sums
 #pragma unroll
         for (int e = 0; e < ChromaAcc<F>::NP; ++e) ca.u[e] = ca.v[e] = 0u;
-        double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;  // identical in all lanes
+        // item sums of the flushed units' H_Y and L: warp totals in every lane, or (VCA_XRED8) per-lane
+        // running sums reduced across lanes once at the item end
+        double sHY = 0.0, sLY = 0.0, sLU = 0.0, sLV = 0.0;
         double *HYrow = a.s.HY + (int64_t)f * CY + (int64_t)r * cols;
         const int64_t fCY = (int64_t)f * CY;  // global index of the frame's first block (test outputs)
         // strips in chroma-flush windows of SPC: the flush runs once after each window (as its
@@ -1987,12 +2017,14 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
 #endif
                     st_keep(HYrow + cl, Hl, keep);
                 }
+                if (!VCA_XRED8) {
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    Hl += __shfl_xor_sync(0xffffffffu, Hl, o);
-                    LYl += __shfl_xor_sync(0xffffffffu, LYl, o);
-                    LUl += __shfl_xor_sync(0xffffffffu, LUl, o);
-                    LVl += __shfl_xor_sync(0xffffffffu, LVl, o);
+                    for (int o = 16; o > 0; o >>= 1) {
+                        Hl += __shfl_xor_sync(0xffffffffu, Hl, o);
+                        LYl += __shfl_xor_sync(0xffffffffu, LYl, o);
+                        LUl += __shfl_xor_sync(0xffffffffu, LUl, o);
+                        LVl += __shfl_xor_sync(0xffffffffu, LVl, o);
+                    }
                 }
                 sHY += Hl;
                 sLY += LYl;
@@ -2013,6 +2045,17 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
         }
         }
         // ---- item end: fixed-order partials of this warp's units (A7 inputs)
+        if (VCA_XRED8) {
+            // value r = {H_Y, L_Y, H_U, L_U, H_V, L_V}: lane 4 r stores the warp total of value r
+            const double vals[8] = {sHY, sLY, hu, sLU, hv, sLV, 0.0, 0.0};
+            const double tot = xred8(vals, lane);
+            const int r6 = lane >> 2;
+            if ((lane & 3) == 0 && r6 < 6) {
+                const int64_t q = (int64_t)r * kConsumers + u;
+                double *P = a.s.partial + (((int64_t)f * 3 + (r6 >> 1)) * a.s.P + q) * 2 + (r6 & 1);
+                st_keep(P, tot, keep);
+            }
+        } else {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             hu += __shfl_xor_sync(0xffffffffu, hu, o);
@@ -2029,6 +2072,7 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
             st_keep(P1 + 1, sLU, keep);
             st_keep(P2, hv, keep);
             st_keep(P2 + 1, sLV, keep);
+        }
         }
     }
 }
