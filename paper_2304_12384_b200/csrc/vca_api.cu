@@ -285,7 +285,10 @@ int launch_analysis(vca_ctx *ctx, const void *const planes[3], const int64_t pit
                 break;
             }
     const int fin_grid = (n_frames + fa.frames_per_cta - 1) / fa.frames_per_cta;
-    finalize_kernel<<<fin_grid, kFinalizeThreads, 0, st>>>(fa);
+    if (fa.frames_per_cta > 1)
+        finalize_kernel<true><<<fin_grid, kFinalizeThreads, 0, st>>>(fa);
+    else
+        finalize_kernel<false><<<fin_grid, kFinalizeThreads, 0, st>>>(fa);
     VCA_CK(ctx, cudaGetLastError());
     ctx->launches += 1;
     if (prof) {
