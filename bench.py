@@ -153,13 +153,31 @@ def bad_clocks(c):
     return False
 
 
+def host_cpu():
+    """(usable host threads, CPU model) of this process: the affinity mask, not the machine's count."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        n = os.cpu_count() or 1
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return n, model
+
+
 def cpu_oracle_fps(Y, U, V, bd, block, lowpass, target_s=10.0, max_frames=None, threads=None):
     """Time the CPU oracle (as it stands) on a bounded sample; returns (fps, frames, seconds, cores)."""
     import oracle
 
     from paper_2304_12384_b200 import synth
 
-    cores = threads or os.cpu_count() or 1
+    cores = threads or host_cpu()[0]
     npl = synth.as_numpy_planes(Y, U, V)
     F = npl[0].shape[0]
     t0 = time.perf_counter()
@@ -191,7 +209,7 @@ def run_reference(args, rank, world):
     oracle.build()
     cfg_id = 3 if world == 1 else 5
     c = synth.CONFIGS[cfg_id]
-    cores = os.cpu_count() or 1
+    cores, cpu_model = host_cpu()
     # bounded sample of the workload: one frame per host core per step
     n = max(1, min(cores, 16))
     Y, U, V = synth.config_frames(cfg_id, device="cpu", n_frames=n)
@@ -212,7 +230,8 @@ def run_reference(args, rank, world):
         "dtype": "int64+f64", "data": "synthetic (config %d generator, CPU torch)" % cfg_id,
         "config": {"workload": workload + " (bounded sample)", "width": c.width,
                    "height": c.height, "bit_depth": 8, "block": 32, "lowpass": True, "frames_per_step": n},
-        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "paper_context_fps": PAPER_FPS,
     }
@@ -515,6 +534,7 @@ def main():
         ns = min(nfr, 160)
         fps, n, dt, cores = cpu_oracle_fps(Y[:ns].cpu(), U[:ns].cpu(), V[:ns].cpu(), bd, c.block_size, c.lowpass)
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": cores, "kind": "oracle",
+                                "cpu_model": host_cpu()[1],
                                 "sample": "%d frame analyses (repeated passes over the first %d frames of the same "
                                           "workload), %.1f s, OpenMP over frames" % (n, ns, dt)}
         # the same oracle on one host thread (BASELINE.md asks for both)
