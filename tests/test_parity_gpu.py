@@ -190,6 +190,23 @@ def test_analyze_host_matches_device():
     assert np.array_equal(host2, dev[1:])
 
 
+def test_analyze_host_error_leaves_sequence_unchanged():
+    """vca.h: an argument error leaves the context unchanged -- a failed vca_analyze_host between
+    two good calls does not advance the POC or the carried H_Y (records equal one uninterrupted
+    sequence bit for bit)."""
+    from paper_2304_12384_b200 import VcaError
+
+    Yc, Uc, Vc = synth.with_pitch(synth.g_frames(33, 200, 136, 6, 8))
+    whole = records_to_numpy(Analyzer(200, 136, 8, 32, False).analyze(*planes_cuda(Yc, Uc, Vc)))
+    a = Analyzer(200, 136, 8, 32, False)
+    first = a.analyze_host(Yc[:3], Uc[:3], Vc[:3], chunk_frames=2)
+    with pytest.raises(VcaError) as e:
+        a.analyze_host(Yc[3:4], Uc[3:4], Vc[3:4], n_halo=1)  # n_frames < 1 + n_halo
+    assert e.value.code == -1
+    rest = a.analyze_host(Yc[3:], Uc[3:], Vc[3:], chunk_frames=2)
+    assert np.array_equal(np.concatenate([first, rest]), whole)
+
+
 def test_argument_errors_gpu():
     from paper_2304_12384_b200 import VcaError
 
