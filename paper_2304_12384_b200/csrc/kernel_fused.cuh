@@ -8,8 +8,9 @@
 // One persistent CTA per SM, warp-specialised (3 consumer groups; 4 for the n = 8 families):
 //
 //  * warpgroup 0: producers (setmaxnreg.dec).  Warp g's elected lane feeds consumer
-//    group g: per strip one 3-D tensor-map load per plane box (swizzled, zero-filled out
-//    of bounds) into the group's ring of smem stages, full/empty mbarriers (A1);
+//    group g: per strip one 4-D tensor-map load per plane (all of the strip's boxes; 3-D
+//    loads per box where the geometry does not allow it), swizzled, zero-filled out of
+//    bounds, into the group's ring of smem stages, full/empty mbarriers (A1);
 //  * warpgroups 1..G: consumer groups of 4 warps (setmaxnreg.inc), each walking its own
 //    item sequence; warp u owns units u + 4n (n < NU) of every strip.  A consumer reads
 //    its units from smem with clamped row/column indices (edge replication, A2),
@@ -27,7 +28,9 @@
 //  * the epilogue (A5, A6, R-2, R-3): luma |C_ij| x w_n(i,j)/(4096 n) in FP64 per
 //    block (needed per block for h), chroma |C| summed exactly per coefficient
 //    position in uint32 and weighted once per flush; per-(frame, row, warp) partial
-//    sums in a fixed order (A7 inputs, R-11).
+//    sums in a fixed order (A7 inputs, R-11), the six per-lane running sums reduced across
+//    the warp once per item by one reduce-scatter (xred8).  The finalize kernel
+//    (kernel_finalize.cuh) turns the partials and the per-block H_Y into records (A7-A9).
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
