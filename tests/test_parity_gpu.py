@@ -207,6 +207,34 @@ def test_analyze_host_error_leaves_sequence_unchanged():
     assert np.array_equal(np.concatenate([first, rest]), whole)
 
 
+def test_contexts_on_concurrent_streams():
+    """vca.h: one context per stream -- two contexts of different families (8-bit low-pass 32,
+    10-bit full 16) launched alternately on two streams, several calls each, give the records of
+    the same calls made one after another on one stream, bit for bit (no state shared between
+    contexts: occupancy caches, tensor maps, scratch, carried H_Y)."""
+    Ya, Ua, Va = planes_cuda(*synth.g_frames(41, 264, 200, 6, 8))
+    Yb, Ub, Vb = planes_cuda(*synth.g_frames(42, 176, 112, 6, 10))
+    ref_a = Analyzer(264, 200, 8, 32, True)
+    ref_b = Analyzer(176, 112, 10, 16, False)
+    want_a = [records_to_numpy(ref_a.analyze(Ya[k:k + 2], Ua[k:k + 2], Va[k:k + 2])) for k in (0, 2, 4)]
+    want_b = [records_to_numpy(ref_b.analyze(Yb[k:k + 2], Ub[k:k + 2], Vb[k:k + 2])) for k in (0, 2, 4)]
+    a = Analyzer(264, 200, 8, 32, True)
+    b = Analyzer(176, 112, 10, 16, False)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs_a = [torch.empty((2, 8), dtype=torch.float64, device="cuda") for _ in range(3)]
+    outs_b = [torch.empty((2, 8), dtype=torch.float64, device="cuda") for _ in range(3)]
+    scr_a = torch.empty(a.scratch_bytes(2) // 8 + 1, dtype=torch.float64, device="cuda")
+    scr_b = torch.empty(b.scratch_bytes(2) // 8 + 1, dtype=torch.float64, device="cuda")
+    for i, k in enumerate((0, 2, 4)):
+        a.analyze(Ya[k:k + 2], Ua[k:k + 2], Va[k:k + 2], out=outs_a[i], scratch=scr_a, stream=s1)
+        b.analyze(Yb[k:k + 2], Ub[k:k + 2], Vb[k:k + 2], out=outs_b[i], scratch=scr_b, stream=s2)
+    torch.cuda.synchronize()
+    for i in range(3):
+        assert np.array_equal(records_to_numpy(outs_a[i]), want_a[i])
+        assert np.array_equal(records_to_numpy(outs_b[i]), want_b[i])
+
+
 def test_argument_errors_gpu():
     from paper_2304_12384_b200 import VcaError
 
