@@ -970,6 +970,18 @@ __device__ __forceinline__ double xred8(const double (&v)[8], int lane)
     return n;
 }
 
+#ifdef VCA_TIMES
+// diagnostic build only (tools/group_times.py): per consumer group, globaltimer at its first
+// wait and after its last item
+__device__ unsigned long long vca_group_t[2][4096];
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 // ------------------------------------------------------------------ kernel
 struct FusedArgs {
     int n_frames;
@@ -1835,6 +1847,9 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
     const int s_fast = cols_whole > last_c ? (cols_whole - last_c - 1) / F::UNITS + 1 : 0;
 
     uint32_t st = 0, phase = 0;
+#ifdef VCA_TIMES
+    if (u == 0 && lane == 0 && vblk < 4096) vca_group_t[0][vblk] = gtimer();
+#endif
 #if VCA_DYN
     const uint32_t hdr0 = smem_off(empty + F::STAGES);
     for (;;) {
@@ -2078,6 +2093,9 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
         }
         }
     }
+#ifdef VCA_TIMES
+    if (u == 0 && lane == 0 && vblk < 4096) vca_group_t[1][vblk] = gtimer();
+#endif
 }
 
 // ------------------------------------------------------------------ host side

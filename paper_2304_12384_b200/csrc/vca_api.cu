@@ -677,6 +677,20 @@ int vca_debug_analyze(vca_ctx *ctx, const void *const planes[3], const int64_t p
     return launch_analysis(ctx, planes, pitch_bytes, frame_stride_bytes, n_frames, n_halo, scratch, out_dev, st, &dp);
 }
 
+#ifdef VCA_TIMES
+// diagnostic build only: copies n pairs (start, end) of per-group globaltimer stamps of the last
+// fused launch to host (ns), starts first
+int vca_debug_group_times(unsigned long long *host, int n)
+{
+    if (!host || n < 0 || n > 4096) return VCA_ERR_INVALID_ARG;
+    if (cudaMemcpyFromSymbol(host, vca_group_t, sizeof(unsigned long long) * n, 0) != cudaSuccess) return VCA_ERR_CUDA;
+    if (cudaMemcpyFromSymbol(host + n, vca_group_t, sizeof(unsigned long long) * n,
+                             sizeof(unsigned long long) * 4096) != cudaSuccess)
+        return VCA_ERR_CUDA;
+    return VCA_OK;
+}
+#endif
+
 int vca_debug_mutate(int plane, int64_t block, int pos, int which)
 {
 #ifdef VCA_MUTATE
