@@ -973,7 +973,7 @@ __device__ __forceinline__ double xred8(const double (&v)[8], int lane)
 #ifdef VCA_TIMES
 // diagnostic build only (tools/group_times.py): per consumer group, globaltimer at its first
 // wait and after its last item
-__device__ unsigned long long vca_group_t[2][4096];
+__device__ unsigned long long vca_group_t[3][4096];  // start, end, SM id
 __device__ __forceinline__ unsigned long long gtimer()
 {
     unsigned long long t;
@@ -1848,7 +1848,12 @@ __global__ void __launch_bounds__(Fam<W_, BD_, LP_>::THREADS, Fam<W_, BD_, LP_>:
 
     uint32_t st = 0, phase = 0;
 #ifdef VCA_TIMES
-    if (u == 0 && lane == 0 && vblk < 4096) vca_group_t[0][vblk] = gtimer();
+    if (u == 0 && lane == 0 && vblk < 4096) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        vca_group_t[0][vblk] = gtimer();
+        vca_group_t[2][vblk] = smid;
+    }
 #endif
 #if VCA_DYN
     const uint32_t hdr0 = smem_off(empty + F::STAGES);

@@ -678,14 +678,17 @@ int vca_debug_analyze(vca_ctx *ctx, const void *const planes[3], const int64_t p
 }
 
 #ifdef VCA_TIMES
-// diagnostic build only: copies n pairs (start, end) of per-group globaltimer stamps of the last
-// fused launch to host (ns), starts first
+// diagnostic build only: copies, for n consumer groups of the last fused launch, the start and
+// end globaltimer stamps (ns) and the SM id, as three arrays of n
 int vca_debug_group_times(unsigned long long *host, int n)
 {
     if (!host || n < 0 || n > 4096) return VCA_ERR_INVALID_ARG;
     if (cudaMemcpyFromSymbol(host, vca_group_t, sizeof(unsigned long long) * n, 0) != cudaSuccess) return VCA_ERR_CUDA;
     if (cudaMemcpyFromSymbol(host + n, vca_group_t, sizeof(unsigned long long) * n,
                              sizeof(unsigned long long) * 4096) != cudaSuccess)
+        return VCA_ERR_CUDA;
+    if (cudaMemcpyFromSymbol(host + 2 * n, vca_group_t, sizeof(unsigned long long) * n,
+                             sizeof(unsigned long long) * 8192) != cudaSuccess)
         return VCA_ERR_CUDA;
     return VCA_OK;
 }
